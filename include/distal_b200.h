@@ -1,0 +1,150 @@
+/*
+ * distal_b200.h -- C ABI of the B200-native distributed dense tensor-algebra path.
+ *
+ * The reference (`tendist`, pure Python) has no FFI; its drop-in boundary for
+ * this path is two-level:
+ *   (1) the leaf-kernel plugin API -- register_leaf_kernel / substitute_leaf /
+ *       LeafRuntime (reference pkg/src/tendist/cin.py:344-379,
+ *       scheduling.py:263-299), whose per-point body is cin.py:399-417
+ *       (_run_leaf) and whose accumulation contract is cin.py:363-365;
+ *   (2) the simulated transfers of execute() phase one
+ *       (reference pkg/src/tendist/simulator.py:563-581 `fetch`, :635-645
+ *       write-back) which on B200 become real NCCL traffic.
+ * Every entry point below replaces one of those; the Python host
+ * (paper_2203_08069_b200/_native.py) binds them with ctypes.
+ *
+ * Conventions
+ *   - All tensors are row-major float64 in device memory owned by the caller
+ *     (PyTorch allocations); leading dimensions / strides are in ELEMENTS.
+ *   - Every call is asynchronous on the given stream (cudaStream_t passed as
+ *     void*; NULL = legacy default stream) and returns int: 0 on success,
+ *     < 0 on failure, with a thread-local message from td_last_error().
+ *   - No C++ exception crosses this ABI; no torch type appears in it.
+ *   - `accumulate` != 0 means OUT += result (the reference's Reduce leaf,
+ *     cin.py:416-417); 0 means OUT = result (Assign, cin.py:414-415).
+ */
+#ifndef DISTAL_B200_H
+#define DISTAL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TD_OK 0
+#define TD_ERR_CUDA (-1)
+#define TD_ERR_NCCL (-2)
+#define TD_ERR_ARG (-3)
+#define TD_ERR_UNSUPPORTED (-4)
+
+/* ---- library / device ------------------------------------------------- */
+/* ABI version (major*10000 + minor*100 + patch). */
+int td_version(void);
+/* Message for the last failing call on this thread ("" if none). */
+const char* td_last_error(void);
+/* Number of visible CUDA devices (0 when no GPU); negative on driver error. */
+int td_device_count(void);
+/* Selects the current device of the calling thread. */
+int td_set_device(int device);
+/* Number of kernel launches this library issued since load (all threads). */
+long long td_launch_count(void);
+
+/* ---- leaf kernels (replace the per-point interpreter, cin.py:399-417) ---- */
+
+/* GEMM leaf  C(i,j) (+)= A(i,k) * B(k,j)   -- statement of algorithms.py:80-83.
+ * Row-major, k contiguous in A, j contiguous in B and C.  FP64 mma.sync DMMA
+ * tiles staged through a cp.async multistage shared-memory pipeline.
+ * Batched form: `batch` independent problems at the given element strides
+ * (strideB may be 0 to share B) -- used for TTM, algorithms.py:300-301. */
+int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K,
+             const double* A, int64_t lda, const double* B, int64_t ldb,
+             double* C, int64_t ldc, int accumulate);
+int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t K,
+                     const double* A, int64_t lda, int64_t strideA,
+                     const double* B, int64_t ldb, int64_t strideB,
+                     double* C, int64_t ldc, int64_t strideC, int accumulate);
+
+/* TTV leaf  A(i,j) (+)= sum_k B(i,j,k) * c(k)   -- algorithms.py:280-281.
+ * Rows (i,j) with element strides (sBi, sBj) in B and (sAi, sAj) in A; k
+ * stride of B and c is 1.  Bandwidth-bound: 128-bit loads, one warp per row,
+ * warp-shuffle row reduction. */
+int td_ttv(void* stream, int64_t I, int64_t J, int64_t K,
+           const double* B, int64_t sBi, int64_t sBj,
+           const double* c, double* A, int64_t sAi, int64_t sAj, int accumulate);
+
+/* TTM leaf  Y(i,j,l) (+)= sum_k B(i,j,k) * C(k,l)   -- algorithms.py:300-301.
+ * Lowered onto the DMMA GEMM (rows (i,j) flattened when contiguous, else
+ * batched over i). */
+int td_ttm(void* stream, int64_t I, int64_t J, int64_t K, int64_t L,
+           const double* B, int64_t sBi, int64_t sBj,
+           const double* C, int64_t ldc,
+           double* Y, int64_t sYi, int64_t sYj, int accumulate);
+
+/* MTTKRP leaf  A(i,j) (+)= sum_{k,l} B(i,k,l) * C(k,j) * D(l,j)
+ * -- algorithms.py:339-340.  Fused: T = B(i,k,:) . D on DMMA tiles, epilogue
+ * multiplies by C(k,:) and reduces over k inside the CTA (deterministic, no
+ * atomics).  l stride of B is 1; j stride of A, C, D is 1. */
+int td_mttkrp(void* stream, int64_t I, int64_t K, int64_t L, int64_t R,
+              const double* B, int64_t sBi, int64_t sBk,
+              const double* C, int64_t ldc, const double* D, int64_t ldd,
+              double* A, int64_t lda, int accumulate);
+
+/* innerprod leaf  a (+)= sum B(x) * C(x) over a rows x n box
+ * -- algorithms.py:320 and the 3-order form.
+ * Rows at element strides sB / sC (contiguous within a row).  Deterministic
+ * two-pass reduction: per-CTA partials into `work` (>= td_innerprod_work_size()
+ * doubles), then one CTA sums them in fixed order into *out. */
+int td_innerprod(void* stream, int64_t rows, int64_t n,
+                 const double* B, int64_t sB, const double* C, int64_t sC,
+                 double* out, double* work, int accumulate);
+int64_t td_innerprod_work_size(void);
+
+/* Generic exact-order nest evaluator: runs an arbitrary leaf statement over
+ * an arbitrary loop nest (split / divide / rotate relations, guards) with the
+ * reference interpreter's per-point accumulation order (cin.py:420-477).
+ * `prog` points to a host struct td_nest_prog (csrc/interp.cuh), `bytes` its
+ * size; it is copied into the launch. */
+int td_nest_eval(void* stream, const void* prog, int64_t bytes);
+
+/* ---- data movement helpers (tiles, commits, packing) ----------------- */
+/* dst[box] (+)= src[box] for an n-d box (ndim <= 8), element strides. */
+int td_copy_box(void* stream, int ndim, const int64_t* shape,
+                double* dst, const int64_t* dst_strides,
+                const double* src, const int64_t* src_strides, int accumulate);
+/* fill a contiguous range with a constant */
+int td_fill(void* stream, double* dst, int64_t n, double value);
+/* Synthetic input generator: writes the box [origin, origin+shape) of a
+ * global tensor with dims `gdims` into dst (row-major, strides dst_strides).
+ * Value at global linear index g: mode 0 -> integer in [-4,4],
+ * mode 1 -> uniform(-1,1); both from splitmix64(seed, tensor_id, g)
+ * (numpy twin: oracle/generator.py). */
+int td_generate(void* stream, int ndim, const int64_t* gdims, const int64_t* origin,
+                const int64_t* shape, double* dst, const int64_t* dst_strides,
+                uint64_t seed, uint64_t tensor_id, int mode);
+
+/* ---- NCCL over NVLink: the lowering of communicate / rotate --------------
+ * (reference simulator.py:563-581 fetch events, :635-645 write-back events) */
+#define TD_UNIQUE_ID_BYTES 128
+int td_nccl_version(void);
+int td_comm_unique_id(char* out /* TD_UNIQUE_ID_BYTES */);
+/* one rank per process: comm over nranks GPUs, this process is `rank` on `device` */
+int td_comm_init_rank(void** comm, int nranks, int rank, const char* unique_id, int device);
+/* single process driving ndev devices */
+int td_comm_init_all(void** comms, int ndev, const int* devices);
+int td_comm_destroy(void* comm);
+int td_group_start(void);
+int td_group_end(void);
+/* point-to-point transfer of `count` float64 (one CommEvent) */
+int td_send(void* comm, void* stream, const double* buf, int64_t count, int peer);
+int td_recv(void* comm, void* stream, double* buf, int64_t count, int peer);
+/* broadcast / sum-reduce / sum-allreduce of float64 over the communicator */
+int td_bcast(void* comm, void* stream, double* buf, int64_t count, int root);
+int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count, int root);
+int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DISTAL_B200_H */

@@ -1,0 +1,45 @@
+// Library-level entry points: version, errors, devices, launch counter.
+#include "common.cuh"
+#include <cstring>
+
+namespace td {
+static thread_local char t_err[1024] = {0};
+std::atomic<long long> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+void clear_error() { t_err[0] = 0; }
+}  // namespace td
+
+extern "C" {
+
+int td_version(void) { return 10000; }  // 1.0.0
+
+const char* td_last_error(void) { return td::t_err; }
+
+int td_device_count(void) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (e != cudaSuccess) {
+    td::set_error("cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    return TD_ERR_CUDA;
+  }
+  return n;
+}
+
+int td_set_device(int device) {
+  TD_CUDA(cudaSetDevice(device));
+  return TD_OK;
+}
+
+long long td_launch_count(void) { return td::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// NCCL over NVLink 5 / NVSwitch: the lowering of the reference's simulated
+// transfers.  Each compute-phase CommEvent (reference
+// pkg/src/tendist/simulator.py:563-581, write-backs :635-645) becomes one
+// ncclSend/ncclRecv pair inside the step's ncclGroupStart/End, issued on the
+// per-GPU communication stream so it overlaps the previous step's leaf
+// kernels; fan-outs and reductions also have ncclBroadcast / ncclReduce forms.
+// Links against the NCCL that PyTorch ships (nvidia-nccl-cu12, 2.28.x) so the
+// process holds a single libnccl.
+#include "common.cuh"
+#include <nccl.h>
+#include <cstring>
+
+#define TD_NCCL(call)                                                          \
+  do {                                                                         \
+    ncclResult_t _r = (call);                                                  \
+    if (_r != ncclSuccess) {                                                   \
+      td::set_error("%s failed: %s", #call, ncclGetErrorString(_r));           \
+      return TD_ERR_NCCL;                                                      \
+    }                                                                          \
+  } while (0)
+
+static_assert(sizeof(ncclUniqueId) == TD_UNIQUE_ID_BYTES, "ncclUniqueId size");
+
+extern "C" {
+
+int td_nccl_version(void) {
+  int v = 0;
+  if (ncclGetVersion(&v) != ncclSuccess) return TD_ERR_NCCL;
+  return v;
+}
+
+int td_comm_unique_id(char* out) {
+  ncclUniqueId id;
+  TD_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return TD_OK;
+}
+
+int td_comm_init_rank(void** comm, int nranks, int rank, const char* unique_id, int device) {
+  TD_REQUIRE(comm && unique_id && nranks > 0 && rank >= 0 && rank < nranks, "comm_init_rank: bad arguments");
+  TD_CUDA(cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t c;
+  TD_NCCL(ncclCommInitRank(&c, nranks, id, rank));
+  *comm = c;
+  return TD_OK;
+}
+
+int td_comm_init_all(void** comms, int ndev, const int* devices) {
+  TD_REQUIRE(comms && devices && ndev > 0, "comm_init_all: bad arguments");
+  ncclComm_t* cs = reinterpret_cast<ncclComm_t*>(comms);
+  TD_NCCL(ncclCommInitAll(cs, ndev, devices));
+  return TD_OK;
+}
+
+int td_comm_destroy(void* comm) {
+  if (!comm) return TD_OK;
+  TD_NCCL(ncclCommDestroy(static_cast<ncclComm_t>(comm)));
+  return TD_OK;
+}
+
+int td_group_start(void) {
+  TD_NCCL(ncclGroupStart());
+  return TD_OK;
+}
+
+int td_group_end(void) {
+  TD_NCCL(ncclGroupEnd());
+  return TD_OK;
+}
+
+int td_send(void* comm, void* stream, const double* buf, int64_t count, int peer) {
+  TD_NCCL(ncclSend(buf, (size_t)count, ncclDouble, peer, static_cast<ncclComm_t>(comm), td::as_stream(stream)));
+  return TD_OK;
+}
+
+int td_recv(void* comm, void* stream, double* buf, int64_t count, int peer) {
+  TD_NCCL(ncclRecv(buf, (size_t)count, ncclDouble, peer, static_cast<ncclComm_t>(comm), td::as_stream(stream)));
+  return TD_OK;
+}
+
+int td_bcast(void* comm, void* stream, double* buf, int64_t count, int root) {
+  TD_NCCL(ncclBroadcast(buf, buf, (size_t)count, ncclDouble, root, static_cast<ncclComm_t>(comm),
+                        td::as_stream(stream)));
+  return TD_OK;
+}
+
+int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count, int root) {
+  TD_NCCL(ncclReduce(send, recv, (size_t)count, ncclDouble, ncclSum, root, static_cast<ncclComm_t>(comm),
+                     td::as_stream(stream)));
+  return TD_OK;
+}
+
+int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count) {
+  TD_NCCL(ncclAllReduce(send, recv, (size_t)count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm),
+                        td::as_stream(stream)));
+  return TD_OK;
+}
+
+}  // extern "C"

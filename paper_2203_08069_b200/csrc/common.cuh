@@ -1,0 +1,49 @@
+// Shared plumbing of the C ABI: thread-local error text, status macros,
+// launch accounting.  See include/distal_b200.h for the conventions.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <atomic>
+#include "../../include/distal_b200.h"
+
+namespace td {
+
+void set_error(const char* fmt, ...);
+void clear_error();
+extern std::atomic<long long> g_launches;
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return TD_ERR_CUDA;
+  }
+  return TD_OK;
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace td
+
+#define TD_CUDA(call)                                                          \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      td::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e),    \
+                    __FILE__, __LINE__);                                       \
+      return TD_ERR_CUDA;                                                      \
+    }                                                                          \
+  } while (0)
+
+#define TD_REQUIRE(cond, ...)                                                  \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      td::set_error(__VA_ARGS__);                                              \
+      return TD_ERR_ARG;                                                       \
+    }                                                                          \
+  } while (0)

@@ -1,0 +1,279 @@
+// FP64 GEMM / TTM leaf kernels (DMMA m8n8k4 tiles, cp.async multistage smem).
+//
+// Replaces the reference's per-point evaluation of the GEMM leaf
+// C(i,j) += A(i,k) * B(k,j) (reference pkg/src/tendist/algorithms.py:80-83,
+// evaluated point by point at cin.py:399-417) and the TTM leaf
+// Y(i,j,l) += B(i,j,k) * C(k,l) (algorithms.py:300-301).
+//
+// Kernel shape (BM x BN x 16 CTA tile, warps of WM x WN):
+//   * STAGES-deep cp.async ring: A tile [BM][16+4], B tile [16][BN+4]
+//     (row pads of 4 doubles make every fragment LDS.64 conflict-free:
+//     rows r=0..3 x cols c=0..3 land on 16 distinct 8-byte banks);
+//   * each warp owns (WM/8) x (WN/8) accumulators of DMMA.8x8x4 in
+//     registers and issues all of them per k4 slice;
+//   * grouped tile rasterisation (8 M-tiles per group) for L2 reuse;
+//   * epilogue writes (or accumulates into) row-major C with bounds checks.
+// Summation order: k tiles ascending, within a tile the DMMA's own order --
+// exact on integer-valued data, |err| <= gamma_K |A||B| on real data.
+#include "common.cuh"
+#include "dmma.cuh"
+
+namespace td {
+
+constexpr int GEMM_BK = 16;
+constexpr int PAD = 4;
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int WARPS_M = BM / WM;
+  static constexpr int WARPS_N = BN / WN;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int SA = GEMM_BK + PAD;  // A row stride (doubles)
+  static constexpr int SB = BN + PAD;       // B row stride (doubles)
+  static constexpr int A_STAGE = BM * SA;
+  static constexpr int B_STAGE = GEMM_BK * SB;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+  static constexpr int FM = WM / 8;
+  static constexpr int FN = WN / 8;
+};
+
+struct GemmArgs {
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+  int accumulate;
+  int tiles_m, tiles_n;
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+dgemm_kernel(GemmArgs p) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
+  extern __shared__ __align__(128) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_STAGE;
+
+  // grouped rasterisation
+  const int tile = blockIdx.x;
+  const int group = 8;
+  const int per_group = group * p.tiles_n;
+  const int g = tile / per_group;
+  const int first_m = g * group;
+  const int gsize = min(p.tiles_m - first_m, group);
+  const int in_g = tile % per_group;
+  const int tm = first_m + in_g % gsize;
+  const int tn = in_g / gsize;
+  const int64_t m0 = int64_t(tm) * BM;
+  const int64_t n0 = int64_t(tn) * BN;
+
+  const int64_t bz = blockIdx.y;
+  const double* __restrict__ A = p.A + bz * p.sA;
+  const double* __restrict__ B = p.B + bz * p.sB;
+  double* __restrict__ C = p.C + bz * p.sC;
+  const int64_t M = p.M, N = p.N, K = p.K;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp / Cfg::WARPS_N) * WM;
+  const int wn0 = (warp % Cfg::WARPS_N) * WN;
+
+  auto load_tile = [&](int stage, int64_t k0) {
+    double* as = As + stage * Cfg::A_STAGE;
+    double* bs = Bs + stage * Cfg::B_STAGE;
+    constexpr int A_CHUNKS = BM * GEMM_BK / VEC;
+    constexpr int A_PER_ROW = GEMM_BK / VEC;
+#pragma unroll
+    for (int c = tid; c < A_CHUNKS; c += Cfg::THREADS) {
+      const int r = c / A_PER_ROW;
+      const int col = (c % A_PER_ROW) * VEC;
+      const int64_t gm = m0 + r, gk = k0 + col;
+      int valid = 0;
+      const double* src = A;
+      if (gm < M && gk < K) {
+        valid = (int)(K - gk < VEC ? K - gk : VEC);
+        src = A + gm * p.lda + gk;
+      }
+      cp_async_f64<VEC>(as + r * Cfg::SA + col, src, valid);
+    }
+    constexpr int B_CHUNKS = GEMM_BK * BN / VEC;
+    constexpr int B_PER_ROW = BN / VEC;
+#pragma unroll
+    for (int c = tid; c < B_CHUNKS; c += Cfg::THREADS) {
+      const int r = c / B_PER_ROW;
+      const int col = (c % B_PER_ROW) * VEC;
+      const int64_t gk = k0 + r, gn = n0 + col;
+      int valid = 0;
+      const double* src = B;
+      if (gk < K && gn < N) {
+        valid = (int)(N - gn < VEC ? N - gn : VEC);
+        src = B + gk * p.ldb + gn;
+      }
+      cp_async_f64<VEC>(bs + r * Cfg::SB + col, src, valid);
+    }
+  };
+
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = (int)ceil_div(K, GEMM_BK);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_tile(s, int64_t(s) * GEMM_BK);
+    cp_async_commit();
+  }
+
+  const int arow = wm0 + (lane >> 2);
+  const int acol = lane & 3;
+  const int brow = lane & 3;
+  const int bcol = wn0 + (lane >> 2);
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = kt + STAGES - 1;
+      if (nt < ktiles) load_tile(nt % STAGES, int64_t(nt) * GEMM_BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < GEMM_BK; kk += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(arow + i * 8) * Cfg::SA + kk + acol];
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + brow) * Cfg::SB + bcol + j * 8];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+    if (r >= M) continue;
+    double* crow = C + r * p.ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h < N) {
+          double v = acc[i][j][h];
+          if (p.accumulate) v += crow[c + h];
+          crow[c + h] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
+  auto kern = dgemm_kernel<BM, BN, WM, WN, STAGES, VEC>;
+  static bool configured = false;  // attribute is per-device; cheap to re-set
+  (void)configured;
+  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  a.tiles_m = (int)ceil_div(a.M, BM);
+  a.tiles_n = (int)ceil_div(a.N, BN);
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
+  TD_REQUIRE(tiles < (1ll << 31) && batch <= 65535, "dgemm: grid too large (%lld tiles, batch %lld)",
+             (long long)tiles, (long long)batch);
+  dim3 grid((unsigned)tiles, (unsigned)batch);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(a);
+  return check_launch("dgemm_kernel");
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, double* C, int64_t ldc,
+                        int64_t sC, int accumulate);
+
+int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a) {
+  if (a.M <= 0 || a.N <= 0 || batch <= 0) return TD_OK;
+  if (a.K <= 0) return zero_or_keep(st, batch, a.M, a.N, a.C, a.ldc, a.sC, a.accumulate);
+  const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
+                    (batch == 1 || (a.sA % 2 == 0 && a.sB % 2 == 0));
+  if (a.N <= 32) {
+    return vec2 ? launch_gemm<256, 32, 32, 32, 4, 2>(st, batch, a)
+                : launch_gemm<256, 32, 32, 32, 4, 1>(st, batch, a);
+  }
+  if (a.N <= 64) {
+    return vec2 ? launch_gemm<256, 64, 64, 32, 4, 2>(st, batch, a)
+                : launch_gemm<256, 64, 64, 32, 4, 1>(st, batch, a);
+  }
+  return vec2 ? launch_gemm<128, 128, 64, 32, 4, 2>(st, batch, a)
+              : launch_gemm<128, 128, 64, 32, 4, 1>(st, batch, a);
+}
+
+__global__ void zero_rows_kernel(double* C, int64_t M, int64_t N, int64_t ldc, int64_t sC) {
+  const int64_t b = blockIdx.y;
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    C[b * sC + (e / N) * ldc + e % N] = 0.0;
+  }
+}
+
+static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, double* C, int64_t ldc,
+                        int64_t sC, int accumulate) {
+  if (accumulate) return TD_OK;
+  const int64_t total = M * N;
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), (unsigned)batch);
+  zero_rows_kernel<<<grid, 256, 0, st>>>(C, M, N, ldc, sC);
+  return check_launch("zero_rows_kernel");
+}
+
+}  // namespace td
+
+extern "C" {
+
+int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+             const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
+  return td::dgemm_dispatch(td::as_stream(stream), 1, a);
+}
+
+int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t K, const double* A,
+                     int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
+                     double* C, int64_t ldc, int64_t strideC, int accumulate) {
+  td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0};
+  int64_t done = 0;
+  while (done < batch) {  // grid.y is limited to 65535
+    const int64_t chunk = std::min<int64_t>(batch - done, 65535);
+    td::GemmArgs c = a;
+    c.A += done * strideA;
+    c.B += done * strideB;
+    c.C += done * strideC;
+    int rc = td::dgemm_dispatch(td::as_stream(stream), chunk, c);
+    if (rc) return rc;
+    done += chunk;
+  }
+  return TD_OK;
+}
+
+int td_ttm(void* stream, int64_t I, int64_t J, int64_t K, int64_t L, const double* B, int64_t sBi,
+           int64_t sBj, const double* C, int64_t ldc, double* Y, int64_t sYi, int64_t sYj,
+           int accumulate) {
+  // Y(i,j,:) = B(i,j,:) . C : rows (i,j) of B times C[K x L].
+  if (sBi == J * sBj && sYi == J * sYj) {  // (i,j) rows flatten into one M = I*J GEMM
+    return td_dgemm(stream, I * J, L, K, B, sBj, C, ldc, Y, sYj, accumulate);
+  }
+  return td_dgemm_batched(stream, I, J, L, K, B, sBj, sBi, C, ldc, 0, Y, sYj, sYi, accumulate);
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""Leaf-kernel numerics on the B200 through the C ABI.
+
+Each native leaf is compared with the oracle's definition of the same
+contraction (oracle/contractions.py, a numpy restatement of the reference
+leaf statements): bit-exact on integer-valued inputs in [-4, 4] (all partial
+sums < 2**53), and within gamma_K * (|A||B|) on uniform(-1, 1) inputs,
+gamma_K = K u / (1 - K u), u = 2**-53 (the north star's "1e-10 scaled by the
+reduction length" is looser than this).
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import contractions as ref
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+U = 2.0 ** -53
+
+
+def gamma(k):
+    return k * U / (1 - k * U)
+
+
+def ints(rng, *shape):
+    return rng.integers(-4, 5, size=shape).astype(np.float64)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.fixture(scope="module")
+def nat():
+    from paper_2203_08069_b200 import _native
+    _native.load()
+    return _native
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (8, 8, 4), (37, 53, 29), (128, 128, 16),
+                                   (257, 129, 100), (300, 64, 1024), (1000, 33, 77),
+                                   (513, 300, 515)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_dgemm_integer_exact(nat, m, n, k, accumulate):
+    rng = np.random.default_rng(m * 1000 + n * 10 + k)
+    a, b, c0 = ints(rng, m, k), ints(rng, k, n), ints(rng, m, n)
+    ta, tb, tc = dev(a), dev(b), dev(c0)
+    nat.call("td_dgemm", stream(), m, n, k, ptr(ta), k, ptr(tb), n, ptr(tc), n, accumulate)
+    want = ref.gemm(a, b) + (c0 if accumulate else 0)
+    assert np.array_equal(tc.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("m,n,k", [(129, 131, 33), (64, 200, 2048)])
+def test_dgemm_strided_views_scalar_path(nat, m, n, k):
+    """Odd leading dimensions / offsets take the 8-byte cp.async path."""
+    rng = np.random.default_rng(7)
+    big_a, big_b = ints(rng, m + 3, k + 5), ints(rng, k + 2, n + 7)
+    big_c = np.zeros((m + 1, n + 3))
+    ta, tb, tc = dev(big_a), dev(big_b), dev(big_c)
+    pa = C.c_void_p(ta.data_ptr() + 8 * (1 * (k + 5) + 3))
+    pb = C.c_void_p(tb.data_ptr() + 8 * (1 * (n + 7) + 1))
+    pc = C.c_void_p(tc.data_ptr() + 8 * 1)
+    nat.call("td_dgemm", stream(), m, n, k, pa, k + 5, pb, n + 7, pc, n + 3, 0)
+    want = ref.gemm(big_a[1:1 + m, 3:3 + k], big_b[1:1 + k, 1:1 + n])
+    got = tc.cpu().numpy()
+    assert np.array_equal(got[:m, 1:1 + n], want)
+    assert not got[m:, :].any() and not got[:, :1].any()
+
+
+def test_dgemm_real_tolerance(nat):
+    rng = np.random.default_rng(3)
+    m, n, k = 300, 260, 1500
+    a, b = rng.uniform(-1, 1, (m, k)), rng.uniform(-1, 1, (k, n))
+    ta, tb = dev(a), dev(b)
+    tc = torch.zeros(m, n, dtype=torch.float64, device="cuda")
+    nat.call("td_dgemm", stream(), m, n, k, ptr(ta), k, ptr(tb), n, ptr(tc), n, 0)
+    want = ref.gemm(a, b)
+    bound = gamma(k) * (np.abs(a) @ np.abs(b))
+    assert np.all(np.abs(tc.cpu().numpy() - want) <= bound)
+
+
+def test_dgemm_batched(nat):
+    rng = np.random.default_rng(5)
+    bsz, m, n, k = 5, 33, 64, 40
+    a, b = ints(rng, bsz, m, k), ints(rng, k, n)
+    ta, tb = dev(a), dev(b)
+    tc = torch.zeros(bsz, m, n, dtype=torch.float64, device="cuda")
+    nat.call("td_dgemm_batched", stream(), bsz, m, n, k, ptr(ta), k, m * k, ptr(tb), n, 0,
+             ptr(tc), n, m * n, 0)
+    assert np.array_equal(tc.cpu().numpy(), np.stack([ref.gemm(a[q], b) for q in range(bsz)]))
+
+
+@pytest.mark.parametrize("i,j,k", [(1, 1, 1), (6, 5, 4), (7, 5, 3), (33, 17, 2048), (5, 9, 301)])
+def test_ttv_exact(nat, i, j, k):
+    rng = np.random.default_rng(i + j + k)
+    b, c = ints(rng, i, j, k), ints(rng, k)
+    tb, tcv = dev(b), dev(c)
+    ta = torch.zeros(i, j, dtype=torch.float64, device="cuda")
+    nat.call("td_ttv", stream(), i, j, k, ptr(tb), j * k, k, ptr(tcv), ptr(ta), j, 1, 0)
+    assert np.array_equal(ta.cpu().numpy(), ref.ttv(b, c))
+
+
+@pytest.mark.parametrize("i,j,k,l", [(5, 4, 6, 3), (3, 7, 33, 64), (16, 16, 128, 64), (2, 3, 5, 70)])
+def test_ttm_exact(nat, i, j, k, l):
+    rng = np.random.default_rng(i * j + k * l)
+    b, cm = ints(rng, i, j, k), ints(rng, k, l)
+    tb, tcm = dev(b), dev(cm)
+    ty = torch.zeros(i, j, l, dtype=torch.float64, device="cuda")
+    nat.call("td_ttm", stream(), i, j, k, l, ptr(tb), j * k, k, ptr(tcm), l, ptr(ty), j * l, l, 0)
+    assert np.array_equal(ty.cpu().numpy(), ref.ttm(b, cm))
+
+
+@pytest.mark.parametrize("i,k,l,r", [(6, 5, 3, 4), (5, 7, 2, 3), (4, 130, 40, 32), (3, 200, 17, 45),
+                                     (2, 256, 1024, 32)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_mttkrp_exact(nat, i, k, l, r, accumulate):
+    rng = np.random.default_rng(i + k + l + r)
+    b, cm, d, a0 = ints(rng, i, k, l), ints(rng, k, r), ints(rng, l, r), ints(rng, i, r)
+    tb, tcm, td, ta = dev(b), dev(cm), dev(d), dev(a0)
+    nat.call("td_mttkrp", stream(), i, k, l, r, ptr(tb), k * l, l, ptr(tcm), r, ptr(td), r,
+             ptr(ta), r, accumulate)
+    want = ref.mttkrp(b, cm, d) + (a0 if accumulate else 0)
+    assert np.array_equal(ta.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("rows,n", [(1, 1), (6, 5), (7, 5), (1, 100003), (33, 4099), (64, 65536)])
+def test_innerprod_exact(nat, rows, n):
+    rng = np.random.default_rng(rows + n)
+    b, c = ints(rng, rows, n), ints(rng, rows, n)
+    tb, tcv = dev(b), dev(c)
+    out = torch.full((1,), 5.0, dtype=torch.float64, device="cuda")
+    work = torch.empty(nat.lib().td_innerprod_work_size(), dtype=torch.float64, device="cuda")
+    nat.call("td_innerprod", stream(), rows, n, ptr(tb), n, ptr(tcv), n, ptr(out), ptr(work), 1)
+    assert out.item() == 5.0 + ref.innerprod(b, c)
+
+
+def test_generate_matches_numpy_twin(nat):
+    from oracle.generator import generate_box
+    dims, origin, shape = (7, 9, 11), (2, 3, 4), (4, 5, 6)
+    for mode in (0, 1):
+        t = torch.empty(shape, dtype=torch.float64, device="cuda")
+        nat.call("td_generate", stream(), 3, nat.i64_array(dims), nat.i64_array(origin),
+                 nat.i64_array(shape), ptr(t), nat.i64_array(t.stride()), 13, 2, mode)
+        assert np.array_equal(t.cpu().numpy(), generate_box(dims, origin, shape, 13, 2, mode))
+
+
+def test_copy_box_and_accumulate(nat):
+    rng = np.random.default_rng(1)
+    src, dst = ints(rng, 6, 7, 8), ints(rng, 5, 9, 4)
+    ts, td = dev(src), dev(dst)
+    shape = (3, 4, 2)
+    s_off = (1 * 56 + 2 * 8 + 5)
+    d_off = (2 * 36 + 1 * 4 + 1)
+    for acc in (0, 1):
+        before = td.cpu().numpy()
+        nat.call("td_copy_box", stream(), 3, nat.i64_array(shape),
+                 C.c_void_p(td.data_ptr() + 8 * d_off), nat.i64_array(td.stride()),
+                 C.c_void_p(ts.data_ptr() + 8 * s_off), nat.i64_array(ts.stride()), acc)
+        want = before.copy()
+        blk = src[1:4, 2:6, 5:7]
+        want[2:5, 1:5, 1:3] = want[2:5, 1:5, 1:3] + blk if acc else blk
+        assert np.array_equal(td.cpu().numpy(), want)
