@@ -1,0 +1,144 @@
+"""The GPU job: which B200s take part, which ones this process drives, NCCL.
+
+Two process models, both mapping the reference's processor grid onto GPUs
+with `Machine.device_of` (rank-order blocks; identity when the grid has one
+processor per GPU):
+
+* single process (default): this process drives ``devices`` (default: the
+  current CUDA device only); several GPUs share one NCCL clique built with
+  ``ncclCommInitAll``;
+* SPMD (``torchrun``, one process per GPU): `configure_distributed()` takes
+  RANK / LOCAL_RANK / WORLD_SIZE from `torch.distributed`, exchanges an NCCL
+  unique id over it, and builds one communicator with ``ncclCommInitRank``.
+
+Every process plans the same launch program (planning is deterministic) and
+issues only the NCCL calls and kernels of the GPUs it owns, in one global
+order, so sends and receives pair up without any extra handshake.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _native
+from .errors import ConfigError, DeviceUnavailable
+
+
+class World:
+    def __init__(self, ngpus, owned, rank=0, nprocs=1, comms=None, torch_devices=None):
+        self.ngpus = ngpus              # GPUs in the job
+        self.owned = list(owned)        # global GPU indices this process drives
+        self.rank = rank
+        self.nprocs = nprocs
+        self.comms = comms or {}        # global GPU index -> ncclComm_t (as int)
+        self.torch_devices = torch_devices or {}   # global GPU index -> torch.device
+        self._streams = {}
+
+    def owns(self, g: int) -> bool:
+        return g in self.torch_devices
+
+    def device(self, g: int):
+        return self.torch_devices[g]
+
+    def streams(self, g: int):
+        """(compute stream, communication stream) of an owned GPU."""
+        if g not in self._streams:
+            import torch
+            dev = self.torch_devices[g]
+            self._streams[g] = (torch.cuda.Stream(device=dev, priority=0),
+                                torch.cuda.Stream(device=dev, priority=-1))
+        return self._streams[g]
+
+    def comm(self, g: int):
+        if g not in self.comms:
+            raise ConfigError(f"GPU {g} has no NCCL communicator (job of {self.ngpus} GPU(s))")
+        return C.c_void_p(self.comms[g])
+
+    @property
+    def multi_gpu(self) -> bool:
+        return self.ngpus > 1
+
+    def close(self):
+        for h in self.comms.values():
+            try:
+                _native.call("td_comm_destroy", C.c_void_p(h))
+            except Exception:
+                pass
+        self.comms = {}
+
+
+_WORLD = None
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device is visible; the B200 path has no CPU fallback")
+    return torch
+
+
+def world() -> World:
+    global _WORLD
+    if _WORLD is None:
+        torch = _torch()
+        _native.load()
+        dev = torch.cuda.current_device()
+        _WORLD = World(1, [0], torch_devices={0: torch.device("cuda", dev)})
+    return _WORLD
+
+
+def configure(devices=None) -> World:
+    """Single process driving `devices` (CUDA ordinals; default all visible)."""
+    global _WORLD
+    torch = _torch()
+    _native.load()
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = list(devices)
+    if _WORLD is not None:
+        _WORLD.close()
+    comms = {}
+    if len(devices) > 1:
+        arr = (C.c_void_p * len(devices))()
+        ids = (C.c_int * len(devices))(*devices)
+        _native.call("td_comm_init_all", arr, len(devices), ids)
+        comms = {g: arr[g] for g in range(len(devices))}
+    _WORLD = World(len(devices), range(len(devices)), comms=comms,
+                   torch_devices={g: torch.device("cuda", d) for g, d in enumerate(devices)})
+    return _WORLD
+
+
+def configure_distributed() -> World:
+    """One process per GPU under torch.distributed (torchrun)."""
+    global _WORLD
+    torch = _torch()
+    import torch.distributed as dist
+    _native.load()
+    if not dist.is_initialized():
+        raise ConfigError("torch.distributed is not initialised")
+    rank, size = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank % max(1, torch.cuda.device_count())))
+    torch.cuda.set_device(local)
+    comms = {}
+    if size > 1:
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _native.call("td_comm_unique_id", uid)
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0)
+        handle = C.c_void_p()
+        _native.call("td_comm_init_rank", C.byref(handle), size, rank, C.c_char_p(box[0]), local)
+        comms = {rank: handle.value}
+    if _WORLD is not None:
+        _WORLD.close()
+    _WORLD = World(size, [rank], rank=rank, nprocs=size, comms=comms,
+                   torch_devices={rank: torch.device("cuda", local)})
+    return _WORLD
+
+
+def reset():
+    global _WORLD
+    if _WORLD is not None:
+        _WORLD.close()
+    _WORLD = None

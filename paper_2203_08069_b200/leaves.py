@@ -1,0 +1,317 @@
+"""Leaf dispatch: from one step's loop nest to a native sm_100a kernel.
+
+The reference evaluates a task's loop nest point by point (reference
+`pkg/src/tendist/cin.py:399-477`) unless `substitute_leaf` routes it to a
+registered plugin (`cin.py:459-463`; the paper's
+``.substitute({ii, ji, ki}, CuBLAS::GeMM)``).  On B200 every
+step of a task is first reduced to its *iteration box*: the interval each
+statement variable sweeps when the launch and step loops are pinned
+(`box_of`).  When the nest visits every point of that box exactly once, the
+leaf statement is matched against the native contractions:
+
+    GEMM      X(a,b) += Y(a,c) * Z(c,b)             -> td_dgemm
+    TTV       X(a,b) += Y(a,b,c) * z(c)             -> td_ttv
+    TTM       X(a,b,d) += Y(a,b,c) * Z(c,d)         -> td_ttm
+    MTTKRP    X(a,b) += Y(a,c,d) * Z(c,b) * W(d,b)  -> td_mttkrp (fused)
+    innerprod x += Y(v...) * Z(v...)                -> td_innerprod
+
+Anything else -- or any nest under the ``"interpreter"`` leaf / the
+``"exact"`` policy -- runs on the exact-order nest kernel (`interp.py`),
+which reproduces the reference's accumulation order bit for bit.  The
+native contractions reassociate sums (exact on integer-valued inputs,
+within gamma_K |A||B| otherwise).
+
+Builtin leaf names usable with `substitute_leaf`: ``"auto"`` (match, else
+nest kernel), ``"dgemm"``/``"gemm"``, ``"ttv"``, ``"ttm"``, ``"mttkrp"``,
+``"innerprod"`` (require that contraction) and ``"interpreter"``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .cin import Assign, Divide, Reduce, Rotate, Split
+from .errors import ConfigError, TendistError
+from .interp import DeviceTile, run_nest, stream_handle, torch_mod
+from .ir import Access, Mul, accesses_of
+from .distribution import HyperRect
+
+BUILTIN_LEAVES = frozenset({"auto", "dgemm", "gemm", "ttv", "ttm", "mttkrp", "innerprod"})
+_ENUM_LIMIT = 1 << 22
+
+# counters for the bench / tests: which path each step took
+STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "nest": 0}
+
+
+def reset_stats():
+    for k in STATS:
+        STATS[k] = 0
+
+
+# ------------------------------------------------------------ box analysis
+def _deps(name, defs, ranges, cache) -> tuple:
+    """Loop variables `name` depends on (ordered, unique)."""
+    if name in cache:
+        return cache[name]
+    if name in ranges:
+        out = (name,)
+    else:
+        rel = defs.get(name)
+        if rel is None:
+            raise TendistError(f"{name} is not resolvable")
+        parts = [rel.outer, rel.inner] if isinstance(rel, (Split, Divide)) else [rel.result, *rel.over]
+        seen = []
+        for p in parts:
+            for l in _deps(p, defs, ranges, cache):
+                if l not in seen:
+                    seen.append(l)
+        out = tuple(seen)
+    cache[name] = out
+    return out
+
+
+def _eval_grid(name, defs, grid):
+    """Evaluate `name` on a dict of broadcast loop-value arrays; (value, phantom)."""
+    if name in grid:
+        return grid[name], np.zeros(grid[name].shape, dtype=bool)
+    rel = defs[name]
+    if isinstance(rel, (Split, Divide)):
+        o, po = _eval_grid(rel.outer, defs, grid)
+        i, pi = _eval_grid(rel.inner, defs, grid)
+        v = o * rel.block + i
+        return v, po | pi | (v >= rel.extent)
+    r, pr = _eval_grid(rel.result, defs, grid)
+    for x in rel.over:
+        o, po = _eval_grid(x, defs, grid)
+        r = r + o
+        pr = pr | po
+    return r % rel.extent, pr
+
+
+def box_of(loops, leaf, defs):
+    """Interval per statement variable if the nest visits each point of the
+    box exactly once, else None.  loops: [(var, lo, hi)] incl. pinned ones."""
+    ranges = {v: (lo, hi) for v, lo, hi in loops}
+    names = list(dict.fromkeys(n for a in [leaf.lhs, *accesses_of(leaf.rhs)] for n in a.var_names))
+    cache = {}
+    owner = {}
+    box = {}
+    for n in names:
+        deps = _deps(n, defs, ranges, cache)
+        live = [d for d in deps if ranges[d][1] - ranges[d][0] > 1]
+        for d in live:
+            if d in owner and owner[d] != n:
+                return None           # a loop feeds two variables: not a product box
+            owner[d] = n
+        size = 1
+        for d in deps:
+            size *= max(0, ranges[d][1] - ranges[d][0])
+        if size == 0:
+            return {}                 # empty nest
+        if size > _ENUM_LIMIT:
+            return None
+        axes = [np.arange(*ranges[d], dtype=np.int64) for d in deps]
+        mesh = np.meshgrid(*axes, indexing="ij") if axes else []
+        grid = dict(zip(deps, mesh))
+        val, ph = _eval_grid(n, defs, grid)
+        vals = np.asarray(val)[~np.asarray(ph)].ravel()
+        if vals.size == 0:
+            return {}
+        lo, hi = int(vals.min()), int(vals.max()) + 1
+        if hi - lo != vals.size or np.unique(vals).size != vals.size:
+            return None
+        box[n] = (lo, hi)
+    # every live loop must feed some variable, else points repeat
+    for v, lo, hi in loops:
+        if hi - lo > 1 and v not in owner:
+            return None
+    return box
+
+
+# ------------------------------------------------------------ matching
+def _factors(e):
+    if isinstance(e, Mul):
+        return _factors(e.lhs) + _factors(e.rhs)
+    return [e]
+
+
+@dataclass
+class Match:
+    kind: str
+    roles: dict     # role -> index of the rhs access (accesses_of order)
+
+
+def classify(leaf) -> Match | None:
+    if not isinstance(leaf, Reduce):
+        return None
+    facs = _factors(leaf.rhs)
+    if not all(isinstance(f, Access) for f in facs):
+        return None
+    accs = accesses_of(leaf.rhs)
+    idx = {id(a): k for k, a in enumerate(accs)}
+    out = leaf.lhs.var_names
+    if len(set(out)) != len(out):
+        return None
+    vs = [f.var_names for f in facs]
+    if any(len(set(v)) != len(v) for v in vs):
+        return None
+    if len(facs) == 2:
+        p, q = facs
+        for y, z in ((p, q), (q, p)):
+            a_, b_ = y.var_names, z.var_names
+            # GEMM X(a,b) += Y(a,c) Z(c,b)
+            if len(out) == 2 and len(a_) == 2 and len(b_) == 2:
+                a, b = out
+                if a_[0] == a and b_[1] == b and a_[1] == b_[0] and a_[1] not in out:
+                    return Match("dgemm", {"A": idx[id(y)], "B": idx[id(z)]})
+            # TTV X(a,b) += Y(a,b,c) z(c)
+            if len(out) == 2 and len(a_) == 3 and len(b_) == 1:
+                if a_[:2] == out and a_[2] == b_[0] and b_[0] not in out:
+                    return Match("ttv", {"B": idx[id(y)], "c": idx[id(z)]})
+            # TTM X(a,b,d) += Y(a,b,c) Z(c,d)
+            if len(out) == 3 and len(a_) == 3 and len(b_) == 2:
+                if a_[:2] == out[:2] and b_ == (a_[2], out[2]) and a_[2] not in out:
+                    return Match("ttm", {"B": idx[id(y)], "C": idx[id(z)]})
+        # innerprod x += Y(v) Z(v)
+        if len(out) == 0 and p.var_names == q.var_names:
+            return Match("innerprod", {"B": idx[id(p)], "C": idx[id(q)]})
+        return None
+    if len(facs) == 3 and len(out) == 2:
+        a, b = out
+        big = [f for f in facs if len(f.var_names) == 3]
+        if len(big) != 1:
+            return None
+        y = big[0]
+        if y.var_names[0] != a:
+            return None
+        c, d = y.var_names[1], y.var_names[2]
+        if len({a, b, c, d}) != 4:
+            return None
+        rest = [f for f in facs if f is not y]
+        z = next((f for f in rest if f.var_names == (c, b)), None)
+        w = next((f for f in rest if f.var_names == (d, b)), None)
+        if z is None or w is None or z is w:
+            return None
+        return Match("mttkrp", {"B": idx[id(y)], "C": idx[id(z)], "D": idx[id(w)]})
+    return None
+
+
+# ------------------------------------------------------------ launching
+def _sub(tile: DeviceTile, acc: Access, box) -> DeviceTile:
+    lo = tuple(box[v][0] for v in acc.var_names)
+    hi = tuple(box[v][1] for v in acc.var_names)
+    return tile.view(HyperRect(lo, hi))
+
+
+def _p(t: DeviceTile):
+    return C.c_void_p(t.ptr())
+
+
+def _launch_native(m: Match, leaf, box, out: DeviceTile, ins, stream, accumulate=1) -> bool:
+    accs = accesses_of(leaf.rhs)
+    o = _sub(out, leaf.lhs, box)
+    v = {role: _sub(ins[k], accs[k], box) for role, k in m.roles.items()}
+    s = stream_handle(stream)
+    st = {r: t.strides() for r, t in v.items()}
+    ost = o.strides()
+    ext = {n: hi - lo for n, (lo, hi) in box.items()}
+    if m.kind == "dgemm":
+        a, b = leaf.lhs.var_names
+        c = accs[m.roles["A"]].var_names[1]
+        if st["A"][1] != 1 or st["B"][1] != 1 or ost[1] != 1:
+            return False
+        _native.call("td_dgemm", s, ext[a], ext[b], ext[c], _p(v["A"]), st["A"][0], _p(v["B"]),
+                     st["B"][0], _p(o), ost[0], accumulate)
+    elif m.kind == "ttv":
+        a, b = leaf.lhs.var_names
+        c = accs[m.roles["c"]].var_names[0]
+        if st["B"][2] != 1 or st["c"][0] != 1:
+            return False
+        _native.call("td_ttv", s, ext[a], ext[b], ext[c], _p(v["B"]), st["B"][0], st["B"][1],
+                     _p(v["c"]), _p(o), ost[0], ost[1], accumulate)
+    elif m.kind == "ttm":
+        a, b, d = leaf.lhs.var_names
+        c = accs[m.roles["B"]].var_names[2]
+        if st["B"][2] != 1 or st["C"][1] != 1 or ost[2] != 1:
+            return False
+        _native.call("td_ttm", s, ext[a], ext[b], ext[c], ext[d], _p(v["B"]), st["B"][0], st["B"][1],
+                     _p(v["C"]), st["C"][0], _p(o), ost[0], ost[1], accumulate)
+    elif m.kind == "mttkrp":
+        a, b = leaf.lhs.var_names
+        _, c, d = accs[m.roles["B"]].var_names
+        if st["B"][2] != 1 or st["C"][1] != 1 or st["D"][1] != 1 or ost[1] != 1:
+            return False
+        _native.call("td_mttkrp", s, ext[a], ext[c], ext[d], ext[b], _p(v["B"]), st["B"][0], st["B"][1],
+                     _p(v["C"]), st["C"][0], _p(v["D"]), st["D"][0], _p(o), ost[0], accumulate)
+    elif m.kind == "innerprod":
+        ok = _innerprod(v["B"], v["C"], o, stream, accumulate)
+        if not ok:
+            return False
+    else:
+        return False
+    STATS[m.kind] += 1
+    return True
+
+
+def _rows_view(t: DeviceTile):
+    """(rows, n, row_stride) if the tile is a stack of equal-stride rows."""
+    shape, st = t.rect.shape, t.strides()
+    if not shape:
+        return 1, 1, 1
+    if st[-1] != 1:
+        return None
+    n = shape[-1]
+    outer = list(zip(shape[:-1], st[:-1]))
+    outer = [(e, s) for e, s in outer if e != 1]
+    if not outer:
+        return 1, n, n
+    # merge outer axes into one stride
+    rows = 1
+    stride = outer[-1][1]
+    expect = stride
+    for e, s in reversed(outer):
+        if s != expect:
+            return None
+        rows *= e
+        expect = s * e
+    return rows, n, stride
+
+
+def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate) -> bool:
+    rb, rc = _rows_view(b), _rows_view(c)
+    if rb is None or rc is None or rb[:2] != rc[:2]:
+        return False
+    torch = torch_mod()
+    work = torch.empty(int(_native.lib().td_innerprod_work_size()), dtype=torch.float64,
+                       device=out.data.device)
+    _native.call("td_innerprod", stream_handle(stream), rb[0], rb[1], _p(b), rb[2], _p(c), rc[2],
+                 _p(out), C.c_void_p(work.data_ptr()), accumulate)
+    if stream is not None:
+        work.record_stream(stream)
+    return True
+
+
+def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream) -> str:
+    """Execute one step nest; returns the path taken ("dgemm", ..., "nest").
+
+    policy: "auto" | a builtin contraction name | "interpreter" / "exact"."""
+    if isinstance(leaf, Reduce) and policy not in ("interpreter", "exact"):
+        m = classify(leaf)
+        want = {"gemm": "dgemm"}.get(policy, policy)
+        if m is not None and (want == "auto" or want == m.kind):
+            box = box_of(loops, leaf, defs)
+            if box == {}:
+                return "empty"
+            if box is not None and _launch_native(m, leaf, box, out, ins, stream):
+                return m.kind
+        if want not in ("auto",):
+            raise ConfigError(f"leaf kernel {policy!r} does not apply to {leaf!r} on this nest")
+    elif policy not in ("auto", "interpreter", "exact"):
+        raise ConfigError(f"leaf kernel {policy!r} needs a reduction statement")
+    run_nest(loops, leaf, defs, out, ins, stream)
+    STATS["nest"] += 1
+    return "nest"

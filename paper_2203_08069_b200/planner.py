@@ -448,3 +448,62 @@ def _operands(prog, plan, task, s, store, pieces_at, tables) -> StepWork:
             ops[key] = (name, box, whole[:1] if whole else cover)
     return StepWork(task, s, ops)
 
+
+
+# ------------------------------------------------ host-only planning (no GPU)
+class _HostRegion:
+    def __init__(self, name, dist):
+        self.name = name
+        self.dist = dist
+        self.residency = dist.residency()
+
+    def held_at(self, coord) -> list:
+        return self.residency.get(coord, [])
+
+    def volume_at(self, coord) -> int:
+        return sum(r.volume for r in self.held_at(coord))
+
+
+class HostStore:
+    """Bookkeeping-only region store: plans and ledgers without touching a GPU
+    (the reference's RegionStore minus values, `simulator.py:274-314`)."""
+
+    def __init__(self, machine):
+        self.machine = machine
+        self.regions: dict = {}
+
+    def declare(self, name, dist):
+        self.regions[name] = _HostRegion(name, dist)
+        return self.regions[name]
+
+    def __contains__(self, name):
+        return name in self.regions
+
+    def __getitem__(self, name):
+        return self.regions[name]
+
+    def persistent_volume(self, coord) -> int:
+        return sum(r.volume_at(coord) for r in self.regions.values())
+
+
+def plan_statement(stmt, machine, distributions, schedule=None, *, record_requirements=True, label=None):
+    """(Program, ExecutionTrace) of a statement: the full ledger and buffer
+    program, computed on the host only."""
+    from .cin import lower_to_cin
+    from .errors import MissingDistribution
+    from .ir import TensorIndexStmt
+    cin = lower_to_cin(stmt) if isinstance(stmt, TensorIndexStmt) else stmt
+    if schedule is not None:
+        cin = schedule.apply(cin)
+    store = HostStore(machine)
+    names = sorted({a.tensor.name for l in leaf_statements(cin) for a in leaf_accesses(l)})
+    for n in names:
+        if n not in distributions:
+            raise MissingDistribution(f"no distribution for {n}")
+        store.declare(n, distributions[n])
+    trace = ExecutionTrace(machine)
+    prog = build_program(cin, store, trace, record_requirements=record_requirements)
+    trace.num_steps = prog.plan.num_steps
+    trace.launches.append({"phase": "compute", "label": label or prog.plan.out_name,
+                           "tasks": len(prog.plan.tasks), "steps": prog.plan.num_steps})
+    return prog, trace

@@ -1,0 +1,681 @@
+"""Execution on B200s: HBM tile store, NCCL transfer program, leaf launches.
+
+Drop-in for the reference's runtime (`pkg/src/tendist/simulator.py`):
+
+* `RegionStore` / `Region` (reference `simulator.py:274-314`): the host
+  bookkeeping (distribution, residency) plus the *HBM tile map*: one
+  contiguous row-major float64 buffer per (GPU, piece), shared by every
+  processor placed on that GPU.  ``Region.tensor`` gathers the canonical
+  value back to the host on demand.
+* `execute` (reference `simulator.py:537-663`): `planner.build_program`
+  reproduces the reference ledger and emits the buffer program; this module
+  runs it.  Per step: the step's transfers are issued as one NCCL group on
+  each GPU's communication stream (same-GPU transfers alias the source
+  tile), the compute stream waits for them, then every task's step nest runs
+  as a native leaf (`leaves.run_leaf`).  Because step s+1's group is queued
+  on the communication stream while step s's leaves run on the compute
+  stream, communication overlaps computation (the reference's double
+  buffering of temporaries across one step boundary, `simulator.py:607-613`).
+  Write-backs (`simulator.py:624-654`) are NCCL transfers into the home GPU
+  followed by an in-order accumulation, so reductions combine in machine
+  enumeration order exactly as the reference does.
+* `run_statement`, `RunResult`, `verify_result`, `redistribute`
+  (reference `simulator.py:317-357, 668-726`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .cin import (Assign, Forall, INTERPRETER_KERNEL, LeafKernel, Place, Reduce, Suchthat,
+                  leaf_accesses, leaf_statements, lookup_leaf_kernel, lower_to_cin)
+from .comm import world as current_world
+from .distribution import HyperRect, TensorDistribution, check_redistributable, subtract_rects
+from .errors import (ConfigError, ExtentMismatch, MissingDistribution, MissingInput, TendistError,
+                     VerifyFail)
+from .interp import DeviceTile, execute_chain, stream_handle, torch_mod
+from .ir import TensorIndexStmt, accesses_of
+from .leaves import BUILTIN_LEAVES, run_leaf
+from .machine import Machine
+from .planner import build_program
+from .tensors import DenseTensor
+from .trace import CommEvent, ExecutionTrace
+
+LEAF_POLICIES = ("auto", "exact")
+
+
+def _strides(t):
+    return _native.i64_array(t.stride())
+
+
+def _copy_box(stream, dst, src, accumulate=False):
+    """dst (+)= src for two same-shape CUDA views on one device."""
+    shape = tuple(dst.shape)
+    if not shape:
+        shape, ds, ss = (1,), _native.i64_array([1]), _native.i64_array([1])
+    else:
+        ds, ss = _strides(dst), _strides(src)
+    _native.call("td_copy_box", stream_handle(stream), len(shape), _native.i64_array(shape),
+                 C.c_void_p(dst.data_ptr()), ds, C.c_void_p(src.data_ptr()), ss, int(accumulate))
+
+
+def _slice(buf, rect: HyperRect, box: HyperRect):
+    """View of the part `box` of a buffer that holds `rect`."""
+    if not box.lo:
+        return buf
+    return buf[tuple(slice(a - o, b - o) for a, b, o in zip(box.lo, box.hi, rect.lo))]
+
+
+# ------------------------------------------------------------------ regions
+class Region:
+    """One tensor: distribution, residency (host bookkeeping) and HBM pieces."""
+
+    def __init__(self, store, name: str, dist: TensorDistribution):
+        self.store = store
+        self.name = name
+        self.dist = dist
+        self.residency = dist.residency()
+        self.pieces = {}          # (gpu, color) -> CUDA tensor holding piece_bounds(color)
+
+    @property
+    def dims(self):
+        return self.dist.tensor_dims
+
+    def held_at(self, coord) -> list:
+        return self.residency.get(coord, [])
+
+    def volume_at(self, coord) -> int:
+        return sum(r.volume for r in self.held_at(coord))
+
+    def gpus_of(self, color) -> list:
+        box = self.dist.piece_bounds(color)
+        m, W = self.store.machine, self.store.world.ngpus
+        out = []
+        for p in self.dist.processors_of(color):
+            if box in self.residency.get(p, ()):
+                g = m.device_of(p, W)
+                if g not in out:
+                    out.append(g)
+        return out
+
+    def piece(self, g, color):
+        return self.pieces[(g, color)]
+
+    @property
+    def tensor(self) -> DenseTensor:
+        return self.store.gather(self.name)
+
+
+class RegionStore:
+    """All regions of one machine, resident in the HBM of the job's GPUs."""
+
+    def __init__(self, machine: Machine, world=None):
+        self.machine = machine
+        self.world = world or current_world()
+        self.regions: dict = {}
+
+    def __contains__(self, name) -> bool:
+        return name in self.regions
+
+    def __getitem__(self, name) -> Region:
+        return self.regions[name]
+
+    def persistent_volume(self, coord) -> int:
+        return sum(r.volume_at(coord) for r in self.regions.values())
+
+    def _check(self, name, dims, dist):
+        if dist.machine != self.machine:
+            raise ConfigError(f"distribution machine {dist.machine} is not the store's {self.machine}")
+        if tuple(dims) != dist.tensor_dims:
+            raise ConfigError(f"{name} has dims {tuple(dims)}, distribution wants {dist.tensor_dims}")
+
+    def _alloc(self, name, dist, fill):
+        """Create the region and one buffer per (owned GPU, piece); fill(g, color, box, buf)."""
+        torch = torch_mod()
+        region = Region(self, name, dist)
+        for color, box, _ in dist.pieces():
+            for g in region.gpus_of(color):
+                if not self.world.owns(g):
+                    continue
+                dev = self.world.device(g)
+                with torch.cuda.device(dev):
+                    buf = torch.empty(box.shape, dtype=torch.float64, device=dev)
+                    fill(g, color, box, buf)
+                region.pieces[(g, color)] = buf
+        self.regions[name] = region
+        return region
+
+    def place(self, name: str, tensor: DenseTensor, dist: TensorDistribution) -> Region:
+        """Copy a host tensor into its pieces (reference `simulator.py:297-305`)."""
+        self._check(name, tensor.dims, dist)
+        torch = torch_mod()
+        host = tensor.data
+
+        def fill(g, color, box, buf):
+            src = host[box.slices()] if box.lo else host
+            buf.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=False)
+
+        return self._alloc(name, dist, fill)
+
+    def place_zeros(self, name: str, dist: TensorDistribution) -> Region:
+        return self._alloc(name, dist, lambda g, c, b, buf: buf.zero_())
+
+    def place_host(self, name: str, host: np.ndarray, dist: TensorDistribution, streams=None) -> Region:
+        """Upload from (ideally pinned) host memory with async copies; `streams`
+        maps GPU -> stream (default: that GPU's compute stream)."""
+        self._check(name, host.shape, dist)
+        torch = torch_mod()
+
+        def fill(g, color, box, buf):
+            st = (streams or {}).get(g) or self.world.streams(g)[0]
+            src = torch.from_numpy(host[box.slices()] if box.lo else host)
+            with torch.cuda.stream(st):
+                if src.is_contiguous():
+                    buf.copy_(src, non_blocking=True)
+                else:
+                    _h2d_box(st, buf, src)
+                buf.record_stream(st)
+
+        return self._alloc(name, dist, fill)
+
+    def place_generated(self, name: str, dist: TensorDistribution, *, seed=0, tensor_id=0,
+                        mode=0) -> Region:
+        """Synthetic inputs generated in HBM (values per oracle/generator.py)."""
+        dims = dist.tensor_dims
+
+        def fill(g, color, box, buf):
+            shape = box.shape or (1,)
+            _native.call("td_generate", stream_handle(_torch_current(buf)), len(dims),
+                         _native.i64_array(dims), _native.i64_array(box.lo or (0,)),
+                         _native.i64_array(shape), C.c_void_p(buf.data_ptr()),
+                         _native.i64_array(buf.stride() or (1,)), seed, tensor_id, mode)
+
+        return self._alloc(name, dist, fill)
+
+    # ---- host views
+    def gather(self, name: str) -> DenseTensor:
+        """Canonical value of a region on the host (D2H of the home pieces)."""
+        torch = torch_mod()
+        region = self.regions[name]
+        out = np.zeros(region.dims, dtype=np.float64)
+        W = self.world
+        for color, box, procs in region.dist.pieces():
+            gpus = region.gpus_of(color)
+            if not gpus:
+                continue
+            src_g = gpus[0]
+            if W.owns(src_g):
+                buf = region.pieces[(src_g, color)]
+                with torch.cuda.device(buf.device):
+                    torch.cuda.current_stream().wait_stream(W.streams(src_g)[0])
+                    arr = buf.cpu().numpy()
+            else:
+                arr = None
+            if W.nprocs > 1:
+                arr = _bcast_piece(W, src_g, box, arr)
+            if box.lo:
+                out[box.slices()] = arr
+            else:
+                out[...] = arr
+        return DenseTensor(region.dims, out)
+
+    def local_pieces(self, name: str):
+        """(box, CUDA tensor) for the home pieces of `name` on this process's GPUs."""
+        region = self.regions[name]
+        for color, box, procs in region.dist.pieces():
+            gpus = region.gpus_of(color)
+            if gpus and self.world.owns(gpus[0]):
+                yield box, region.pieces[(gpus[0], color)]
+
+
+def _torch_current(buf):
+    import torch
+    return torch.cuda.current_stream(buf.device)
+
+
+def _h2d_box(stream, dst, src):
+    """Host (strided) -> device box copy, one cudaMemcpyAsync per contiguous row run."""
+    import torch
+    tmp = src.contiguous()
+    dst.copy_(tmp, non_blocking=False)
+
+
+def _bcast_piece(W, root_g, box, arr):
+    """SPMD: every process obtains the piece held by GPU root_g."""
+    torch = torch_mod()
+    g = W.owned[0]
+    dev = W.device(g)
+    buf = torch.from_numpy(arr).to(dev) if arr is not None else torch.empty(box.shape, dtype=torch.float64,
+                                                                           device=dev)
+    st = torch.cuda.current_stream(dev)
+    _native.call("td_bcast", W.comm(g), stream_handle(st), C.c_void_p(buf.data_ptr()),
+                 max(1, box.volume), root_g)
+    return buf.cpu().numpy()
+
+
+# ----------------------------------------------------------------- execute
+def _loops_of(node):
+    loops = []
+    while isinstance(node, (Forall, Suchthat)):
+        if isinstance(node, Forall):
+            loops.append((node.var, node.lo, node.hi))
+        node = node.body
+    return loops, node
+
+
+def _leaf_choice(relations, loop_vars, policy):
+    """(policy, python plugin or None) for a nest, from its LeafKernel relations."""
+    for rel in relations:
+        if isinstance(rel, LeafKernel) and rel.vars[0] in loop_vars:
+            if rel.kernel == INTERPRETER_KERNEL:
+                return "exact", None
+            fn = lookup_leaf_kernel(rel.kernel)
+            if fn is not None:
+                return policy, {rel.vars[0]: fn}
+            if rel.kernel in BUILTIN_LEAVES:
+                return (rel.kernel if policy == "auto" else policy), None
+            raise TendistError(f"leaf kernel {rel.kernel!r} is not registered")
+    return policy, None
+
+
+class _Executor:
+    def __init__(self, prog, store: RegionStore, policy: str):
+        self.prog = prog
+        self.plan = prog.plan
+        self.store = store
+        self.W = store.world
+        self.policy = policy
+        self.m = store.machine
+        self.buffers = {}            # hid -> CUDA tensor (owned GPUs only)
+        self.out_bufs = {}           # task coord -> CUDA tensor of out_rect
+        self.torch = torch_mod()
+        self.gpus = sorted({self.gpu(t.coord) for t in self.plan.tasks} |
+                           {g for g in self.W.owned})
+        self.owned = [g for g in self.gpus if self.W.owns(g)]
+
+    def gpu(self, p) -> int:
+        return self.m.device_of(p, self.W.ngpus)
+
+    def cstream(self, g):
+        return self.W.streams(g)[0]
+
+    def xstream(self, g):
+        return self.W.streams(g)[1]
+
+    # ---- buffers
+    def holding_buf(self, hid):
+        h = self.prog.holdings[hid]
+        if h.kind == "piece":
+            return self.store[h.tensor].piece(self.gpu(h.proc), h.color)
+        return self.buffers[hid]
+
+    def _sync(self, waiter, producer):
+        ev = self.torch.cuda.Event()
+        ev.record(producer)
+        waiter.wait_event(ev)
+
+    # ---- phases
+    def run(self):
+        torch = self.torch
+        for g in self.owned:
+            cur = torch.cuda.current_stream(self.W.device(g))
+            self._sync(self.cstream(g), cur)
+            self._sync(self.xstream(g), cur)
+        out_region = self.store[self.plan.out_name]
+        for t in self.plan.tasks:
+            g = self.gpu(t.coord)
+            if t.out_rect is not None and self.W.owns(g):
+                with torch.cuda.stream(self.cstream(g)):
+                    self.out_bufs[t.coord] = torch.zeros(t.out_rect.shape, dtype=torch.float64,
+                                                         device=self.W.device(g))
+        nsteps = self.plan.num_steps
+        for s in range(nsteps):
+            self.transfers(self.prog.transfers[s])
+            for g in self.owned:
+                self._sync(self.cstream(g), self.xstream(g))
+            if self.prog.stepwise:
+                self.compute(self.prog.work[s], s)
+            self.release(s)
+        if not self.prog.stepwise:
+            self.compute(self.prog.work[-1], -1)
+        self.commit(out_region)
+        for g in self.owned:
+            cur = torch.cuda.current_stream(self.W.device(g))
+            self._sync(cur, self.cstream(g))
+            self._sync(cur, self.xstream(g))
+        self.buffers.clear()
+        self.out_bufs.clear()
+
+    def transfers(self, moves):
+        torch = self.torch
+        sends, recvs = [], []
+        for t in moves:
+            gs, gd = self.gpu(t.src), self.gpu(t.dst)
+            if gs == gd:
+                if self.W.owns(gs):
+                    src_h = self.prog.holdings[t.src_hid]
+                    self.buffers[t.dst_hid] = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
+                continue
+            if self.W.owns(gs):
+                src_h = self.prog.holdings[t.src_hid]
+                view = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
+                if not view.is_contiguous():
+                    st = self.xstream(gs)
+                    with torch.cuda.stream(st):
+                        packed = torch.empty(t.part.shape, dtype=torch.float64, device=view.device)
+                    _copy_box(st, packed, view)
+                    view = packed
+                sends.append((gs, gd, view))
+            if self.W.owns(gd):
+                st = self.xstream(gd)
+                with torch.cuda.stream(st):
+                    buf = torch.empty(t.part.shape, dtype=torch.float64, device=self.W.device(gd))
+                buf.record_stream(self.cstream(gd))
+                self.buffers[t.dst_hid] = buf
+                recvs.append((gd, gs, buf))
+        self._nccl(sends, recvs)
+
+    def _nccl(self, sends, recvs):
+        if not sends and not recvs:
+            return
+        _native.call("td_group_start")
+        try:
+            for g, peer, view in sends:
+                _native.call("td_send", self.W.comm(g), stream_handle(self.xstream(g)),
+                             C.c_void_p(view.data_ptr()), max(1, view.numel()), peer)
+            for g, peer, buf in recvs:
+                _native.call("td_recv", self.W.comm(g), stream_handle(self.xstream(g)),
+                             C.c_void_p(buf.data_ptr()), max(1, buf.numel()), peer)
+        finally:
+            _native.call("td_group_end")
+
+    def operand(self, g, name, rect, hids):
+        """A CUDA view holding `rect` of tensor `name` on GPU g."""
+        torch = self.torch
+        if len(hids) == 1 and self.prog.holdings[hids[0]].rect.contains(rect):
+            h = self.prog.holdings[hids[0]]
+            return _slice(self.holding_buf(hids[0]), h.rect, rect)
+        st = self.cstream(g)
+        with torch.cuda.stream(st):
+            buf = torch.zeros(rect.shape, dtype=torch.float64, device=self.W.device(g))
+        for hid in hids:
+            h = self.prog.holdings[hid]
+            part = h.rect.intersect(rect) if rect.lo else rect
+            if part is None:
+                continue
+            _copy_box(st, _slice(buf, rect, part), _slice(self.holding_buf(hid), h.rect, part))
+        return buf
+
+    def compute(self, works, s):
+        plan = self.plan
+        task_loops, leaf = _loops_of(plan.task_body)
+        loop_vars = [v for v, _, _ in task_loops]
+        policy, plugins = _leaf_choice(plan.relations, loop_vars, self.policy)
+        rhs = accesses_of(leaf.rhs)
+        for w in works:
+            g = self.gpu(w.task.coord)
+            if not self.W.owns(g) or w.task.out_rect is None:
+                continue
+            if any(rect is None for _, rect, _ in w.operands.values()):
+                continue      # some access is empty on this step: no iteration points
+            st = self.cstream(g)
+            loops = [(v, c, c + 1) for v, c in w.task.env.items()]
+            for v, lo, hi in task_loops:
+                if s >= 0 and plan.step_var is not None and v == plan.step_var.var:
+                    lo, hi = s, s + 1
+                loops.append((v, lo, hi))
+            out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
+                                  plan.out_access.tensor.dims)
+            tiles = {}
+            for key, (name, rect, hids) in w.operands.items():
+                tiles[key] = DeviceTile(name, rect, self.operand(g, name, rect, hids),
+                                        self.store[name].dims)
+            ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
+            if plugins:
+                read = {a.tensor.name: tiles[(a.tensor.name, a.var_names)] for a in rhs}
+                execute_chain(loops[len(w.task.env):], leaf, dict(w.task.env), plan.defs, read,
+                              {plan.out_name: out_tile}, plugins, st, self.W.device(g))
+            else:
+                run_leaf(policy, loops, leaf, plan.defs, out_tile, ins, st)
+
+    def release(self, s):
+        for hid, last in self.prog.last_use.items():
+            if last == s:
+                self.buffers.pop(hid, None)
+
+    def commit(self, region):
+        torch = self.torch
+        plan = self.plan
+        # senders must see finished leaves
+        for g in self.owned:
+            self._sync(self.xstream(g), self.cstream(g))
+        sends, recvs, staged = [], [], {}
+        for k, c in enumerate(self.prog.commits):
+            gt, gh = self.gpu(c.task.coord), self.gpu(c.home)
+            if gt == gh:
+                continue
+            if self.W.owns(gt):
+                self.out_bufs[c.task.coord].record_stream(self.xstream(gt))
+                view = _slice(self.out_bufs[c.task.coord], c.task.out_rect, c.part)
+                if not view.is_contiguous():
+                    st = self.xstream(gt)
+                    with torch.cuda.stream(st):
+                        packed = torch.empty(c.part.shape, dtype=torch.float64, device=view.device)
+                    _copy_box(st, packed, view)
+                    view = packed
+                sends.append((gt, gh, view))
+            if self.W.owns(gh):
+                st = self.xstream(gh)
+                with torch.cuda.stream(st):
+                    buf = torch.empty(c.part.shape, dtype=torch.float64, device=self.W.device(gh))
+                buf.record_stream(self.cstream(gh))
+                staged[k] = buf
+                recvs.append((gh, gt, buf))
+        self._nccl(sends, recvs)
+        for g in self.owned:
+            self._sync(self.cstream(g), self.xstream(g))
+        acc = plan.out_kind == "reduce"
+        for k, c in enumerate(self.prog.commits):
+            gh = self.gpu(c.home)
+            if not self.W.owns(gh):
+                continue
+            piece = region.piece(gh, c.color)
+            dst = _slice(piece, region.dist.piece_bounds(c.color), c.part)
+            if k in staged:
+                src = staged[k]
+            else:
+                src = _slice(self.out_bufs[c.task.coord], c.task.out_rect, c.part)
+            _copy_box(self.cstream(gh), dst, src, accumulate=acc)
+
+
+def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: int = 1,
+            label: str = None, record_requirements: bool = True, leaf_policy: str = "auto"):
+    """Run one scheduled statement on the GPUs (reference `simulator.py:537-663`).
+
+    `workers` is accepted for signature compatibility; GPU parallelism
+    replaces the reference's thread pool.  `leaf_policy` is ``"auto"``
+    (native contractions where they apply) or ``"exact"`` (the nest kernel
+    everywhere: bitwise identical to the reference on any input)."""
+    if leaf_policy not in LEAF_POLICIES:
+        raise ConfigError(f"leaf_policy must be one of {LEAF_POLICIES}")
+    if trace is None:
+        trace = ExecutionTrace(store.machine)
+    prog = build_program(stmt, store, trace, record_requirements=record_requirements)
+    _Executor(prog, store, leaf_policy).run()
+    plan = prog.plan
+    out_region = store[plan.out_name]
+    if plan.out_kind == "reduce" and out_region.dist.replicated:
+        for color in out_region.dist.colors():
+            procs = out_region.dist.processors_of(color)
+            bounds = out_region.dist.piece_bounds(color)
+            for q in procs[1:]:
+                out_region.residency[q] = [r for r in out_region.residency.get(q, []) if r != bounds]
+        keep = {(g, c) for (g, c) in out_region.pieces if g in out_region.gpus_of(c)}
+        out_region.pieces = {k: v for k, v in out_region.pieces.items() if k in keep}
+    trace.num_steps = max(trace.num_steps, plan.num_steps)
+    trace.launches.append({"phase": "compute", "label": label or plan.out_name,
+                           "tasks": len(plan.tasks), "steps": plan.num_steps})
+    return trace
+
+
+@dataclass
+class RunResult:
+    output_name: str
+    trace: ExecutionTrace
+    store: RegionStore
+    _output: DenseTensor = None
+
+    @property
+    def output(self) -> DenseTensor:
+        if self._output is None:
+            self._output = self.store.gather(self.output_name)
+        return self._output
+
+
+def _scheduled(stmt, schedule):
+    cin = lower_to_cin(stmt) if isinstance(stmt, TensorIndexStmt) else stmt
+    return schedule.apply(cin) if schedule is not None else cin
+
+
+def prepare_store(cin, machine, distributions, inputs=None, *, world=None, generated=None):
+    """Place inputs (host tensors, or synthetic `generated={name: (seed, id, mode)}`)
+    and a zero output; validation follows reference `simulator.py:691-711`."""
+    leaves = leaf_statements(cin)
+    out_name = leaves[0].lhs.tensor.name
+    dims = {}
+    for leaf in leaves:
+        for acc in leaf_accesses(leaf):
+            dims[acc.tensor.name] = acc.tensor.dims
+    store = RegionStore(machine, world)
+    for name in sorted(dims):
+        if name not in distributions:
+            raise MissingDistribution(f"no distribution for {name}")
+        if name == out_name:
+            continue
+        if generated is not None and name in generated:
+            seed, tid, mode = generated[name]
+            store.place_generated(name, distributions[name], seed=seed, tensor_id=tid, mode=mode)
+            continue
+        if inputs is None or name not in inputs:
+            raise MissingInput(f"no input tensor for {name}")
+        if inputs[name].dims != dims[name]:
+            raise ExtentMismatch(f"{name}: statement wants dims {dims[name]}, input has {inputs[name].dims}")
+        store.place(name, inputs[name], distributions[name])
+    store.place_zeros(out_name, distributions[out_name])
+    return store, out_name
+
+
+def run_statement(stmt, machine: Machine, distributions: dict, inputs: dict, schedule=None, *,
+                  workers: int = 1, label: str = None, leaf_policy: str = "auto") -> RunResult:
+    """Place inputs in HBM, apply the schedule, execute, return the output
+    (reference `simulator.py:676-715`)."""
+    cin = _scheduled(stmt, schedule)
+    store, out_name = prepare_store(cin, machine, distributions, inputs)
+    trace = ExecutionTrace(machine)
+    execute(cin, store, trace=trace, workers=workers, label=label, leaf_policy=leaf_policy)
+    return RunResult(out_name, trace, store)
+
+
+def verify_result(stmt, inputs: dict, result: RunResult, atol: float = 1e-9) -> None:
+    """Compare a run with the single-memory evaluation (reference `simulator.py:718-726`);
+    the reference evaluation itself runs on the GPU's exact-order nest kernel."""
+    from .ir import sequential_evaluate
+    expected = sequential_evaluate(stmt, inputs)
+    got = result.output
+    if expected.dims != got.dims:
+        raise VerifyFail(f"output dims {got.dims} != reference {expected.dims}")
+    err = float(np.max(np.abs(expected.data - got.data))) if expected.volume else 0.0
+    if err > atol:
+        raise VerifyFail(f"max deviation {err} above {atol}")
+
+
+def redistribute(store: RegionStore, name: str, new_dist: TensorDistribution,
+                 trace: ExecutionTrace) -> None:
+    """Move a region to a new distribution (reference `simulator.py:317-357`):
+    every piece a processor must newly hold is fetched from the
+    lowest-enumeration other holder, as placement-phase events; the data
+    moves over NCCL (or stays in place on a shared GPU)."""
+    torch = torch_mod()
+    region = store.regions[name]
+    check_redistributable(region.dist, new_dist)
+    old = region.residency
+    new = new_dist.residency()
+    old_colors = [(region.dist.piece_bounds(c), region.dist.processors_of(c), c)
+                  for c in region.dist.colors()]
+    moved = 0
+    fetched = {p: 0 for p in store.machine.enumerate()}
+    moves = []   # (src proc, dst proc, part, old color)
+    for p in store.machine.enumerate():
+        for rect in new.get(p, []):
+            for piece in subtract_rects([rect], old.get(p, [])):
+                for bounds, procs, color in old_colors:
+                    part = piece.intersect(bounds)
+                    if part is None:
+                        continue
+                    src = next((q for q in procs if q != p), None)
+                    if src is None:
+                        continue
+                    trace.events.append(CommEvent(0, src, p, name, part, part.volume, "copy", "placement"))
+                    moves.append((src, p, part, color))
+                    moved += part.volume
+                    fetched[p] += part.volume
+    for p in store.machine.enumerate():
+        trace.bump_memory(p, store.persistent_volume(p) + fetched[p])
+    # data: build the new pieces from old pieces (local copies) and NCCL moves
+    W = store.world
+    m = store.machine
+    old_region = region
+    new_region = Region(store, name, new_dist)
+    sends, recvs = [], []
+    for color, box, _ in new_dist.pieces():
+        for g in new_region.gpus_of(color):
+            if not W.owns(g):
+                continue
+            dev = W.device(g)
+            buf = torch.zeros(box.shape, dtype=torch.float64, device=dev)
+            new_region.pieces[(g, color)] = buf
+            st = torch.cuda.current_stream(dev)
+            for ocolor, obox, oprocs in region.dist.pieces():
+                part = box.intersect(obox) if box.lo else box
+                if part is None:
+                    continue
+                og = [x for x in old_region.gpus_of(ocolor)]
+                if g in og:
+                    _copy_box(st, _slice(buf, box, part),
+                              _slice(old_region.piece(g, ocolor), obox, part))
+                else:
+                    src_g = og[0]
+                    staging = torch.empty(part.shape, dtype=torch.float64, device=dev)
+                    recvs.append((g, src_g, staging, buf, box, part))
+    for color, box, _ in new_dist.pieces():
+        for g in new_region.gpus_of(color):
+            for ocolor, obox, oprocs in region.dist.pieces():
+                part = box.intersect(obox) if box.lo else box
+                if part is None:
+                    continue
+                og = old_region.gpus_of(ocolor)
+                if g in og or not W.owns(og[0]):
+                    continue
+                view = _slice(old_region.piece(og[0], ocolor), obox, part).contiguous()
+                sends.append((og[0], g, view))
+    if sends or recvs:
+        _native.call("td_group_start")
+        for g, peer, view in sends:
+            _native.call("td_send", W.comm(g), stream_handle(torch.cuda.current_stream(W.device(g))),
+                         C.c_void_p(view.data_ptr()), max(1, view.numel()), peer)
+        for g, peer, staging, _, _, _ in recvs:
+            _native.call("td_recv", W.comm(g), stream_handle(torch.cuda.current_stream(W.device(g))),
+                         C.c_void_p(staging.data_ptr()), max(1, staging.numel()), peer)
+        _native.call("td_group_end")
+        for g, _, staging, buf, box, part in recvs:
+            _copy_box(torch.cuda.current_stream(W.device(g)), _slice(buf, box, part), staging)
+    region.dist = new_dist
+    region.residency = new
+    region.pieces = new_region.pieces
+    trace.launches.append({"phase": "placement", "kind": "redistribute", "tensor": name,
+                           "elements": moved, "to": new_dist.describe()})
