@@ -47,6 +47,11 @@ _ENUM_LIMIT = 1 << 22
 STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "nest": 0}
 
 
+# optional per-launch device timing: set TIMING = [] to collect
+# (kind, start_event, end_event) recorded on the launching stream
+TIMING = None
+
+
 def reset_stats():
     for k in STATS:
         STATS[k] = 0
@@ -295,6 +300,24 @@ def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate
     return True
 
 
+def _timing_start(stream):
+    if TIMING is None:
+        return None
+    torch = torch_mod()
+    ev = torch.cuda.Event(enable_timing=True)
+    ev.record(stream)
+    return ev
+
+
+def _timing_stop(kind, ev, stream):
+    if ev is None:
+        return
+    torch = torch_mod()
+    end = torch.cuda.Event(enable_timing=True)
+    end.record(stream)
+    TIMING.append((kind, ev, end))
+
+
 def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream) -> str:
     """Execute one step nest; returns the path taken ("dgemm", ..., "nest").
 
@@ -306,8 +329,11 @@ def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream) -> st
             box = box_of(loops, leaf, defs)
             if box == {}:
                 return "empty"
-            if box is not None and _launch_native(m, leaf, box, out, ins, stream):
-                return m.kind
+            if box is not None:
+                ev = _timing_start(stream)
+                if _launch_native(m, leaf, box, out, ins, stream):
+                    _timing_stop(m.kind, ev, stream)
+                    return m.kind
         if want not in ("auto",):
             raise ConfigError(f"leaf kernel {policy!r} does not apply to {leaf!r} on this nest")
     elif policy not in ("auto", "interpreter", "exact"):

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -76,11 +77,15 @@ class Region:
     """One tensor: distribution, residency (host bookkeeping) and HBM pieces."""
 
     def __init__(self, store, name: str, dist: TensorDistribution):
-        self.store = store
+        self._store = weakref.ref(store)     # no store<->region cycle: HBM frees on `del store`
         self.name = name
         self.dist = dist
         self.residency = dist.residency()
         self.pieces = {}          # (gpu, color) -> CUDA tensor holding piece_bounds(color)
+
+    @property
+    def store(self):
+        return self._store()
 
     @property
     def dims(self):
@@ -182,6 +187,35 @@ class RegionStore:
                 buf.record_stream(st)
 
         return self._alloc(name, dist, fill)
+
+    def local_colors(self, dist: TensorDistribution):
+        """(color, box) of the pieces some GPU of this process must hold."""
+        probe = Region(self, "?", dist)
+        for color, box, _ in dist.pieces():
+            if any(self.world.owns(g) for g in probe.gpus_of(color)):
+                yield color, box
+
+    def place_local(self, name: str, dist: TensorDistribution, host_pieces: dict) -> Region:
+        """Upload per-piece host arrays (pinned for async H2D): host_pieces maps
+        color -> array of that piece's box.  Only this process's pieces are
+        needed -- the e2e path of the benchmark."""
+        torch = torch_mod()
+
+        def fill(g, color, box, buf):
+            st = self.world.streams(g)[0]
+            with torch.cuda.stream(st):
+                buf.copy_(torch.from_numpy(host_pieces[color]), non_blocking=True)
+            buf.record_stream(st)
+
+        region = self._alloc(name, dist, fill)
+        for g in self.world.owned:
+            torch.cuda.current_stream(self.world.device(g)).wait_stream(self.world.streams(g)[0])
+        return region
+
+    def zero(self, name: str) -> None:
+        """Reset every resident piece of a region to +0.0 (a fresh output)."""
+        for buf in self.regions[name].pieces.values():
+            buf.zero_()
 
     def place_generated(self, name: str, dist: TensorDistribution, *, seed=0, tensor_id=0,
                         mode=0) -> Region:
