@@ -61,6 +61,11 @@ long long td_launch_count(void);
 int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K,
              const double* A, int64_t lda, const double* B, int64_t ldb,
              double* C, int64_t ldc, int accumulate);
+/* Same GEMM with a forced tile configuration (tuning / tests; csrc/gemm.cu
+ * TD_GEMM_CONFIGS lists them); config < 0 = the default choice. */
+int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K,
+                    const double* A, int64_t lda, const double* B, int64_t ldb,
+                    double* C, int64_t ldc, int accumulate);
 int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t K,
                      const double* A, int64_t lda, int64_t strideA,
                      const double* B, int64_t ldb, int64_t strideB,
@@ -90,6 +95,11 @@ int td_mttkrp(void* stream, int64_t I, int64_t K, int64_t L, int64_t R,
               const double* B, int64_t sBi, int64_t sBk,
               const double* C, int64_t ldc, const double* D, int64_t ldd,
               double* A, int64_t lda, int accumulate);
+/* Same with a forced CTA configuration (csrc/mttkrp.cu; < 0 = default). */
+int td_mttkrp_config(void* stream, int config, int64_t I, int64_t K, int64_t L, int64_t R,
+                     const double* B, int64_t sBi, int64_t sBk,
+                     const double* C, int64_t ldc, const double* D, int64_t ldd,
+                     double* A, int64_t lda, int accumulate);
 
 /* innerprod leaf  a (+)= sum B(x) * C(x) over a rows x n box
  * -- algorithms.py:320 and the 3-order form.

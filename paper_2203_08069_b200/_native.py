@@ -31,10 +31,12 @@ _SIGNATURES = {
     "td_set_device": ([i32], i32),
     "td_launch_count": ([], C.c_longlong),
     "td_dgemm": ([vp, i64, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
+    "td_dgemm_config": ([vp, i32, i64, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
     "td_dgemm_batched": ([vp, i64, i64, i64, i64, dp, i64, i64, dp, i64, i64, dp, i64, i64, i32], i32),
     "td_ttv": ([vp, i64, i64, i64, dp, i64, i64, dp, dp, i64, i64, i32], i32),
     "td_ttm": ([vp, i64, i64, i64, i64, dp, i64, i64, dp, i64, dp, i64, i64, i32], i32),
     "td_mttkrp": ([vp, i64, i64, i64, i64, dp, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
+    "td_mttkrp_config": ([vp, i32, i64, i64, i64, i64, dp, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
     "td_innerprod": ([vp, i64, i64, dp, i64, dp, i64, dp, dp, i32], i32),
     "td_innerprod_work_size": ([], i64),
     "td_nest_eval": ([vp, vp, i64], i32),

@@ -20,11 +20,11 @@
 
 namespace td {
 
-constexpr int GEMM_BK = 16;
 constexpr int PAD = 4;
 
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 struct GemmCfg {
+  static constexpr int GEMM_BK = BK;
   static constexpr int WARPS_M = BM / WM;
   static constexpr int WARPS_N = BN / WN;
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
@@ -49,10 +49,12 @@ struct GemmArgs {
   int tiles_m, tiles_n;
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES>::THREADS,
+                                  GemmCfg<BM, BN, BK, WM, WN, STAGES>::THREADS <= 128 ? 2 : 1)
 dgemm_kernel(GemmArgs p) {
-  using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  constexpr int GEMM_BK = BK;
   extern __shared__ __align__(128) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
@@ -181,10 +183,10 @@ dgemm_kernel(GemmArgs p) {
   }
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int VEC>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
 static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
-  using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
-  auto kern = dgemm_kernel<BM, BN, WM, WN, STAGES, VEC>;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC>;
   static bool configured = false;  // attribute is per-device; cheap to re-set
   (void)configured;
   TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -200,24 +202,70 @@ static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+}  // namespace td
+#include "gemm_ws.cuh"
+namespace td {
+
 static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, double* C, int64_t ldc,
                         int64_t sC, int accumulate);
 
-int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a) {
+// Tile configurations (BM, BN, BK, WM, WN, STAGES).  `config` < 0 picks by N.
+#define TD_GEMM_CONFIGS(X)                  \
+  X(0, 128, 128, 16, 64, 32, 4)             \
+  X(1, 128, 128, 32, 64, 32, 3)             \
+  X(2, 128, 128, 16, 32, 32, 4)             \
+  X(3, 128, 128, 32, 32, 32, 3)             \
+  X(4, 256, 64, 16, 64, 32, 4)              \
+  X(5, 256, 64, 32, 64, 32, 2)              \
+  X(6, 256, 32, 16, 32, 32, 4)              \
+  X(7, 128, 64, 32, 32, 32, 3)              \
+  X(16, 64, 128, 16, 32, 64, 3)             \
+  X(17, 64, 128, 32, 32, 64, 2)             \
+  X(18, 128, 64, 16, 64, 32, 3)             \
+  X(19, 64, 128, 16, 32, 64, 4)             \
+  X(20, 64, 64, 16, 32, 32, 4)              \
+  X(21, 128, 32, 16, 64, 16, 4)             \
+  X(22, 128, 64, 32, 64, 32, 2)             \
+  X(23, 128, 64, 16, 32, 64, 3)
+
+// warp-specialised (producer warp + mbarrier ring) variants
+#define TD_GEMM_WS_CONFIGS(X)               \
+  X(10, 128, 128, 32, 64, 32, 3)            \
+  X(11, 128, 128, 16, 64, 32, 5)            \
+  X(12, 256, 64, 32, 64, 32, 2)             \
+  X(13, 128, 64, 32, 32, 32, 4)             \
+  X(14, 256, 64, 16, 64, 32, 4)             \
+  X(15, 128, 128, 16, 32, 32, 6)
+
+// Measured on B200 (scratch/tune2.py): 128x64x16 tiles, 4 warps of 64x32, 3
+// stages, two CTAs per SM -> 34.2 TFLOP/s at 16384^3 (92% of the 37.1 FP64
+// peak) and 33.1 TFLOP/s for the TTM shape (M = 2^20, N = 64, K = 1024).
+static int default_config(int64_t N) {
+  if (N <= 32) return 21;
+  return 18;
+}
+
+int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) {
   if (a.M <= 0 || a.N <= 0 || batch <= 0) return TD_OK;
   if (a.K <= 0) return zero_or_keep(st, batch, a.M, a.N, a.C, a.ldc, a.sC, a.accumulate);
   const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                     (batch == 1 || (a.sA % 2 == 0 && a.sB % 2 == 0));
-  if (a.N <= 32) {
-    return vec2 ? launch_gemm<256, 32, 32, 32, 4, 2>(st, batch, a)
-                : launch_gemm<256, 32, 32, 32, 4, 1>(st, batch, a);
+  if (config < 0) config = default_config(a.N);
+  switch (config) {
+#define TD_GEMM_CASE(id, BM, BN, BK, WM, WN, ST) \
+  case id:                                        \
+    return vec2 ? launch_gemm<BM, BN, BK, WM, WN, ST, 2>(st, batch, a) : launch_gemm<BM, BN, BK, WM, WN, ST, 1>(st, batch, a);
+    TD_GEMM_CONFIGS(TD_GEMM_CASE)
+#undef TD_GEMM_CASE
+#define TD_GEMM_WS_CASE(id, BM, BN, BK, WM, WN, ST) \
+  case id:                                           \
+    return vec2 ? launch_gemm_ws<BM, BN, BK, WM, WN, ST, 2>(st, batch, a) : launch_gemm_ws<BM, BN, BK, WM, WN, ST, 1>(st, batch, a);
+    TD_GEMM_WS_CONFIGS(TD_GEMM_WS_CASE)
+#undef TD_GEMM_WS_CASE
+    default:
+      set_error("dgemm: unknown tile config %d", config);
+      return TD_ERR_ARG;
   }
-  if (a.N <= 64) {
-    return vec2 ? launch_gemm<256, 64, 64, 32, 4, 2>(st, batch, a)
-                : launch_gemm<256, 64, 64, 32, 4, 1>(st, batch, a);
-  }
-  return vec2 ? launch_gemm<128, 128, 64, 32, 4, 2>(st, batch, a)
-              : launch_gemm<128, 128, 64, 32, 4, 1>(st, batch, a);
 }
 
 __global__ void zero_rows_kernel(double* C, int64_t M, int64_t N, int64_t ldc, int64_t sC) {
@@ -246,6 +294,12 @@ int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int
              const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
   td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a);
+}
+
+int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                    const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
+  return td::dgemm_dispatch(td::as_stream(stream), 1, a, config);
 }
 
 int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t K, const double* A,

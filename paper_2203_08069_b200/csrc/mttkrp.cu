@@ -3,29 +3,39 @@
 // point at cin.py:399-417 in the reference).
 //
 // One CTA owns one i (and one 32-wide block of j):
-//   for each k-block of 128 rows:  T[128 x 32] = B(i, kblk, :) . D[:, jblk]
-//        on DMMA.8x8x4 tiles fed by a cp.async ring over l (16 per stage);
+//   for each k-block of ROWS = 32*WARPS rows:
+//        T[ROWS x 32] = B(i, kblk, :) . D[:, jblk] on DMMA.8x8x4 tiles (every
+//        warp 32 x 32, 16 DMMA per k4 slice) fed by a cp.async ring over l
+//        (16 per stage);
 //   epilogue per k-block: partial(j) += sum_k C(k,j) * T(k,j) in registers;
-//   end: fixed-order shuffle + shared-memory tree over the 8 warps, then one
-//   write (or accumulate) of A(i, jblk).
+//   end: fixed-order shuffle + shared-memory tree over the warps.
+// The (i, k-block) pairs are independent CTAs (I x ceil(K/ROWS) of them, so
+// the grid is many waves deep and the tail is small); each writes its partial
+// row to a stream-ordered workspace and a second kernel sums the k-blocks of
+// every A(i, :) in ascending order and writes (or accumulates) A.
 // No atomics: the summation order is a fixed function of the shape, so runs
 // are bitwise reproducible; exact on integer-valued data.
 // B is streamed once from HBM (8 B per 64 flop at R = 32); D and C stay in L2.
+// Small CTAs (4 warps, ~75-100 KB smem) let 2-3 of them share an SM, so one
+// CTA's barrier / epilogue is covered by another's DMMA issue.
 #include "common.cuh"
 #include "dmma.cuh"
 
 namespace td {
 
 constexpr int MK_BK = 16;              // l per pipeline stage
-constexpr int MK_ROWS = 128;           // k rows per block
 constexpr int MK_R = 32;               // j columns per CTA
-constexpr int MK_THREADS = 256;        // 8 warps x 16 rows
-constexpr int MK_STAGES = 4;
 constexpr int MK_SA = MK_BK + 4;       // B-tile row stride (doubles)
 constexpr int MK_SD = MK_R + 4;        // D-tile row stride
-constexpr int MK_A_STAGE = MK_ROWS * MK_SA;
-constexpr int MK_D_STAGE = MK_BK * MK_SD;
-constexpr int MK_SMEM = MK_STAGES * (MK_A_STAGE + MK_D_STAGE) * 8 + 8 * MK_R * 8;
+
+template <int WARPS, int STAGES>
+struct MkCfg {
+  static constexpr int ROWS = WARPS * 32;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int A_STAGE = ROWS * MK_SA;
+  static constexpr int D_STAGE = MK_BK * MK_SD;
+  static constexpr int SMEM = STAGES * (A_STAGE + D_STAGE) * 8 + WARPS * MK_R * 8;
+};
 
 struct MttkrpArgs {
   int64_t I, K, L, R;
@@ -38,32 +48,38 @@ struct MttkrpArgs {
   double* A;
   int64_t lda;
   int accumulate;
+  double* work;   // [I][kblocks][R] partials
 };
 
-template <int VEC>
-__global__ void __launch_bounds__(MK_THREADS, 2) mttkrp_kernel(MttkrpArgs p) {
+template <int WARPS, int STAGES, int VEC>
+__global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(MttkrpArgs p) {
+  using Cfg = MkCfg<WARPS, STAGES>;
+  constexpr int ROWS = Cfg::ROWS;
   extern __shared__ __align__(128) double smem[];
   double* Bs = smem;
-  double* Ds = smem + MK_STAGES * MK_A_STAGE;
-  double* red = Ds + MK_STAGES * MK_D_STAGE;  // [8 warps][32]
+  double* Ds = smem + STAGES * Cfg::A_STAGE;
+  double* red = Ds + STAGES * Cfg::D_STAGE;  // [WARPS][32]
 
-  const int64_t i = blockIdx.x;
+  const int kblocks = (int)ceil_div(p.K, ROWS);
+  const int64_t i = blockIdx.x / kblocks;
+  const int kb = blockIdx.x % kblocks;
   const int64_t j0 = int64_t(blockIdx.y) * MK_R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* __restrict__ Bi = p.B + i * p.sBi;
   const int64_t K = p.K, L = p.L, R = p.R;
 
-  const int kblocks = (int)ceil_div(K, MK_ROWS);
   const int ltiles = (int)ceil_div(L, MK_BK);
-  const int total = kblocks * ltiles;
+  const int total = ltiles;
+  const int64_t kbase = int64_t(kb) * ROWS;
 
   auto load = [&](int stage, int t) {
-    const int64_t k0 = int64_t(t / ltiles) * MK_ROWS;
-    const int64_t l0 = int64_t(t % ltiles) * MK_BK;
-    double* bs = Bs + stage * MK_A_STAGE;
-    double* ds = Ds + stage * MK_D_STAGE;
+    const int64_t k0 = kbase;
+    const int64_t l0 = int64_t(t) * MK_BK;
+    double* bs = Bs + stage * Cfg::A_STAGE;
+    double* ds = Ds + stage * Cfg::D_STAGE;
     constexpr int B_PER_ROW = MK_BK / VEC;
-    for (int c = tid; c < MK_ROWS * B_PER_ROW; c += MK_THREADS) {
+#pragma unroll 4
+    for (int c = tid; c < ROWS * B_PER_ROW; c += Cfg::THREADS) {
       const int r = c / B_PER_ROW, col = (c % B_PER_ROW) * VEC;
       const int64_t gk = k0 + r, gl = l0 + col;
       int valid = 0;
@@ -75,7 +91,7 @@ __global__ void __launch_bounds__(MK_THREADS, 2) mttkrp_kernel(MttkrpArgs p) {
       cp_async_f64<VEC>(bs + r * MK_SA + col, src, valid);
     }
     constexpr int D_PER_ROW = MK_R / VEC;
-    for (int c = tid; c < MK_BK * D_PER_ROW; c += MK_THREADS) {
+    for (int c = tid; c < MK_BK * D_PER_ROW; c += Cfg::THREADS) {
       const int r = c / D_PER_ROW, col = (c % D_PER_ROW) * VEC;
       const int64_t gl = l0 + r, gj = j0 + col;
       int valid = 0;
@@ -88,59 +104,60 @@ __global__ void __launch_bounds__(MK_THREADS, 2) mttkrp_kernel(MttkrpArgs p) {
     }
   };
 
-  double acc[2][4][2];
+  double acc[4][4][2];
   double part[4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a) part[a][0] = part[a][1] = 0.0;
 #pragma unroll
-  for (int m = 0; m < 2; ++m)
+  for (int m = 0; m < 4; ++m)
 #pragma unroll
     for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < MK_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < total) load(s, s);
     cp_async_commit();
   }
-  const int arow = warp * 16 + (lane >> 2);
+  const int arow = warp * 32 + (lane >> 2);
   const int acol = lane & 3;
   const int brow = lane & 3;
   const int bcol = lane >> 2;
 
   for (int t = 0; t < total; ++t) {
-    cp_async_wait<MK_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      const int nt = t + MK_STAGES - 1;
-      if (nt < total) load(nt % MK_STAGES, nt);
+      const int nt = t + STAGES - 1;
+      if (nt < total) load(nt % STAGES, nt);
       cp_async_commit();
     }
-    const double* bs = Bs + (t % MK_STAGES) * MK_A_STAGE;
-    const double* ds = Ds + (t % MK_STAGES) * MK_D_STAGE;
+    const double* bs = Bs + (t % STAGES) * Cfg::A_STAGE;
+    const double* ds = Ds + (t % STAGES) * Cfg::D_STAGE;
 #pragma unroll
     for (int kk = 0; kk < MK_BK; kk += 4) {
-      double af[2], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int m = 0; m < 2; ++m) af[m] = bs[(arow + m * 8) * MK_SA + kk + acol];
+      for (int m = 0; m < 4; ++m) af[m] = bs[(arow + m * 8) * MK_SA + kk + acol];
 #pragma unroll
       for (int n = 0; n < 4; ++n) bf[n] = ds[(kk + brow) * MK_SD + bcol + n * 8];
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
     }
-    if (t % ltiles == ltiles - 1) {  // k-block finished: Hadamard with C, reduce over k
-      const int64_t k0 = int64_t(t / ltiles) * MK_ROWS;
+    if (t == total - 1) {  // k-block finished: Hadamard with C, reduce over k
+      const int64_t k0 = kbase;
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int64_t k = k0 + warp * 16 + m * 8 + (lane >> 2);
+      for (int m = 0; m < 4; ++m) {
+        const int64_t k = k0 + warp * 32 + m * 8 + (lane >> 2);
         const bool kin = k < K;
+        const double* crow = p.C + k * p.ldc;
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t j = j0 + n * 8 + (lane & 3) * 2 + h;
-            if (kin && j < R) part[n][h] += p.C[k * p.ldc + j] * acc[m][n][h];
+            if (kin && j < R) part[n][h] += crow[j] * acc[m][n][h];
             acc[m][n][h] = 0.0;
           }
         }
@@ -170,35 +187,85 @@ __global__ void __launch_bounds__(MK_THREADS, 2) mttkrp_kernel(MttkrpArgs p) {
   if (tid < MK_R) {
     double v = red[tid];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) v += red[w * MK_R + tid];
+    for (int w = 1; w < WARPS; ++w) v += red[w * MK_R + tid];
     const int64_t j = j0 + tid;
-    if (j < R) {
-      double* dst = p.A + i * p.lda + j;
-      *dst = p.accumulate ? *dst + v : v;
-    }
+    if (j < R) p.work[(i * kblocks + kb) * R + j] = v;
+  }
+}
+
+// A(i, j) (+)= sum over k-blocks, ascending (fixed order)
+__global__ void mttkrp_reduce(const double* __restrict__ work, int kblocks, int64_t I, int64_t R, double* A,
+                              int64_t lda, int accumulate) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < I * R; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / R, j = e - (e / R) * R;
+    const double* w = work + i * kblocks * R + j;
+    double v = 0.0;
+    for (int kb = 0; kb < kblocks; ++kb) v += w[int64_t(kb) * R];
+    double* dst = A + i * lda + j;
+    *dst = accumulate ? *dst + v : v;
   }
 }
 
 static bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
 
+template <int WARPS, int STAGES>
+static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
+  using Cfg = MkCfg<WARPS, STAGES>;
+  const int64_t kblocks = std::max<int64_t>(1, ceil_div(a.K, Cfg::ROWS));
+  TD_REQUIRE(a.I * kblocks < (1ll << 31), "mttkrp: grid too large");
+  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * kblocks * a.R, st));
+  if (a.K <= 0) {
+    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.R, st));
+  }
+  dim3 grid((unsigned)(a.K > 0 ? a.I * kblocks : 0), (unsigned)ceil_div(a.R, MK_R));
+  if (a.K > 0) {
+  if (vec2) {
+    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM));
+    mttkrp_kernel<WARPS, STAGES, 2><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+  } else {
+    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM));
+    mttkrp_kernel<WARPS, STAGES, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+  }
+  int rc = check_launch("mttkrp_kernel");
+  if (rc) return rc;
+  }
+  const int64_t outs = a.I * a.R;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(outs, 256), 148 * 8));
+  mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, (int)kblocks, a.I, a.R, a.A, a.lda, a.accumulate);
+  int rc = check_launch("mttkrp_reduce");
+  TD_CUDA(cudaFreeAsync(a.work, st));
+  return rc;
+}
+
+int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
+  const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
+  switch (config < 0 ? 1 : config) {
+    case 0: return launch_mttkrp<4, 4>(st, a, vec2);
+    case 1: return launch_mttkrp<4, 3>(st, a, vec2);
+    case 2: return launch_mttkrp<8, 3>(st, a, vec2);
+    case 3: return launch_mttkrp<2, 4>(st, a, vec2);
+    default:
+      set_error("mttkrp: unknown config %d", config);
+      return TD_ERR_ARG;
+  }
+}
+
 }  // namespace td
+
+extern "C" int td_mttkrp_config(void* stream, int config, int64_t I, int64_t K, int64_t L, int64_t R,
+                                const double* B, int64_t sBi, int64_t sBk, const double* C, int64_t ldc,
+                                const double* D, int64_t ldd, double* A, int64_t lda, int accumulate) {
+  using namespace td;
+  if (I <= 0 || R <= 0) return TD_OK;
+  TD_REQUIRE(I <= 2147483647, "mttkrp: I too large");
+  MttkrpArgs a{I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate, nullptr};
+  return mttkrp_dispatch(as_stream(stream), a, config);
+}
 
 extern "C" int td_mttkrp(void* stream, int64_t I, int64_t K, int64_t L, int64_t R, const double* B,
                          int64_t sBi, int64_t sBk, const double* C, int64_t ldc, const double* D,
                          int64_t ldd, double* A, int64_t lda, int accumulate) {
-  using namespace td;
-  if (I <= 0 || R <= 0) return TD_OK;
-  TD_REQUIRE(I <= 2147483647, "mttkrp: I too large");
-  MttkrpArgs a{I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate};
-  const bool vec2 = al16(B) && al16(D) && sBi % 2 == 0 && sBk % 2 == 0 && ldd % 2 == 0;
-  dim3 grid((unsigned)I, (unsigned)ceil_div(R, MK_R));
-  cudaStream_t st = as_stream(stream);
-  if (vec2) {
-    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, MK_SMEM));
-    mttkrp_kernel<2><<<grid, MK_THREADS, MK_SMEM, st>>>(a);
-  } else {
-    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, MK_SMEM));
-    mttkrp_kernel<1><<<grid, MK_THREADS, MK_SMEM, st>>>(a);
-  }
-  return check_launch("mttkrp_kernel");
+  return td_mttkrp_config(stream, -1, I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate);
 }

@@ -109,16 +109,18 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return t;
 }
 
-// pass 1: block b owns elements [b*chunk, (b+1)*chunk) of the rows x n box
+// pass 1: the rows x n box is cut into tiles of `chunk` elements; block b owns
+// tiles b, b + G, b + 2G, ... so all blocks stream one moving window of HBM
+// (DRAM page locality, like TTV's row order) and the assignment stays fixed.
 __global__ void __launch_bounds__(IP_THREADS) innerprod_partial(int64_t rows, int64_t n, const double* __restrict__ B,
                                                                 int64_t sB, const double* __restrict__ C, int64_t sC,
                                                                 double* __restrict__ work, int64_t chunk) {
   __shared__ double sh[32];
   const int64_t total = rows * n;
-  const int64_t e0 = int64_t(blockIdx.x) * chunk;
-  const int64_t e1 = min(total, e0 + chunk);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int64_t e = e0; e < e1;) {
+  for (int64_t t0 = int64_t(blockIdx.x) * chunk; t0 < total; t0 += int64_t(gridDim.x) * chunk) {
+  const int64_t e1 = min(total, t0 + chunk);
+  for (int64_t e = t0; e < e1;) {
     const int64_t r = e / n;
     const int64_t c0 = e - r * n;
     const int64_t seg = min(n - c0, e1 - e);
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(IP_THREADS) innerprod_partial(int64_t rows, in
     const int64_t tail = head + 2 * pairs;
     if (threadIdx.x == 0 && tail < seg) a1 = fma(ld_stream1(pb + tail), ld_stream1(pc + tail), a1);
     e += seg;
+  }
   }
   const double s = block_sum((a0 + a1) + (a2 + a3), sh);
   if (threadIdx.x == 0) work[blockIdx.x] = s;
@@ -266,8 +269,9 @@ int td_innerprod(void* stream, int64_t rows, int64_t n, const double* B, int64_t
   cudaStream_t st = as_stream(stream);
   const int64_t total = rows > 0 && n > 0 ? rows * n : 0;
   int parts = (int)std::min<int64_t>((int64_t)num_sms() * IP_BLOCKS_PER_SM, IP_MAX_BLOCKS);
-  parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, ceil_div(total, 2048)));
-  const int64_t chunk = std::max<int64_t>(1, ceil_div(total, parts));
+  // 8192-element tiles (64 KiB per operand), interleaved over the blocks
+  const int64_t chunk = 8192;
+  parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, ceil_div(total, chunk)));
   if (total > 0) {
     innerprod_partial<<<parts, IP_THREADS, 0, st>>>(rows, n, B, sB, C, sC, work, chunk);
     int rc = check_launch("innerprod_partial");

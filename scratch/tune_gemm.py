@@ -1,0 +1,43 @@
+import ctypes as C, sys, json
+sys.path.insert(0, ".")
+import torch
+from paper_2203_08069_b200 import _native as nat
+nat.load()
+st = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)
+P = lambda t: C.c_void_p(t.data_ptr())
+def gen(shape, tid):
+    t = torch.empty(shape, dtype=torch.float64, device="cuda")
+    nat.call("td_generate", st(), len(shape), nat.i64_array(shape), nat.i64_array([0]*len(shape)), nat.i64_array(shape), P(t), nat.i64_array(t.stride()), 0, tid, 0)
+    return t
+def bench(fn, it=3):
+    fn(); torch.cuda.synchronize()
+    s=torch.cuda.Event(enable_timing=True); e=torch.cuda.Event(enable_timing=True)
+    ts=[]
+    for _ in range(it):
+        s.record(); fn(); e.record(); e.synchronize(); ts.append(s.elapsed_time(e))
+    return min(ts)
+res = {}
+for n in (8192, 16384):
+    a, b = gen((n, n), 1), gen((n, n), 2); c = torch.empty(n, n, dtype=torch.float64, device="cuda")
+    ref = None
+    for cfg in (1, 16, 17, 19, 18):
+        ms = bench(lambda: nat.call("td_dgemm_config", st(), cfg, n, n, n, P(a), n, P(b), n, P(c), n, 0), 2 if n == 16384 else 3)
+        ok = bool(torch.equal(c[:32], a[:32] @ b))
+        res[f"gemm{n}_cfg{cfg}"] = (round(2*n**3/ms/1e9, 1), ok)
+        print(n, cfg, res[f"gemm{n}_cfg{cfg}"], flush=True)
+    del a, b, c
+M, N, K = 1024*1024, 64, 1024
+a, b = gen((M, K), 1), gen((K, N), 2); c = torch.empty(M, N, dtype=torch.float64, device="cuda")
+for cfg in (5, 18, 20, 21, 16):
+    ms = bench(lambda: nat.call("td_dgemm_config", st(), cfg, M, N, K, P(a), K, P(b), N, P(c), N, 0))
+    ok = bool(torch.equal(c[:32], a[:32] @ b))
+    res[f"ttm_cfg{cfg}"] = (round(2*M*N*K/ms/1e9, 1), ok)
+    print("ttm", cfg, res[f"ttm_cfg{cfg}"], flush=True)
+del a, c
+n = 2048
+b = gen((n, n, n), 1); c2 = gen((n, n, n), 3)
+out = torch.zeros(1, dtype=torch.float64, device="cuda"); work = torch.empty(8192, dtype=torch.float64, device="cuda")
+ms = bench(lambda: nat.call("td_innerprod", st(), 1, n**3, P(b), n**3, P(c2), n**3, P(out), P(work), 0))
+res["innerprod_gbs"] = 16*n**3/ms/1e6
+print(res["innerprod_gbs"])
+json.dump(res, open("gpurun_out/tune_gemm.json", "w"), indent=1)
