@@ -213,6 +213,18 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
   using Cfg = MkCfg<WARPS, STAGES>;
   const int64_t kblocks = std::max<int64_t>(1, ceil_div(a.K, Cfg::ROWS));
   TD_REQUIRE(a.I * kblocks < (1ll << 31), "mttkrp: grid too large");
+  {  // keep the stream-ordered pool's memory across syncs (no re-mapping per call)
+    int dev = 0;
+    TD_CUDA(cudaGetDevice(&dev));
+    static bool retained[64] = {false};
+    if (dev < 64 && !retained[dev]) {
+      cudaMemPool_t pool;
+      TD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t keep = ~0ull;
+      TD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      retained[dev] = true;
+    }
+  }
   TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * kblocks * a.R, st));
   if (a.K <= 0) {
     TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.R, st));

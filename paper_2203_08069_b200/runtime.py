@@ -82,6 +82,7 @@ class Region:
         self.dist = dist
         self.residency = dist.residency()
         self.pieces = {}          # (gpu, color) -> CUDA tensor holding piece_bounds(color)
+        self.zeroed = False       # every piece is known to hold +0.0 (fresh output)
 
     @property
     def store(self):
@@ -168,7 +169,9 @@ class RegionStore:
         return self._alloc(name, dist, fill)
 
     def place_zeros(self, name: str, dist: TensorDistribution) -> Region:
-        return self._alloc(name, dist, lambda g, c, b, buf: buf.zero_())
+        region = self._alloc(name, dist, lambda g, c, b, buf: buf.zero_())
+        region.zeroed = True
+        return region
 
     def place_host(self, name: str, host: np.ndarray, dist: TensorDistribution, streams=None) -> Region:
         """Upload from (ideally pinned) host memory with async copies; `streams`
@@ -216,6 +219,7 @@ class RegionStore:
         """Reset every resident piece of a region to +0.0 (a fresh output)."""
         for buf in self.regions[name].pieces.values():
             buf.zero_()
+        self.regions[name].zeroed = True
 
     def place_generated(self, name: str, dist: TensorDistribution, *, seed=0, tensor_id=0,
                         mode=0) -> Region:
@@ -361,9 +365,14 @@ class _Executor:
             self._sync(self.cstream(g), cur)
             self._sync(self.xstream(g), cur)
         out_region = self.store[self.plan.out_name]
+        self.direct = self._direct_commits(out_region)
         for t in self.plan.tasks:
             g = self.gpu(t.coord)
             if t.out_rect is not None and self.W.owns(g):
+                if t.coord in self.direct:
+                    color = self.direct[t.coord]
+                    self.out_bufs[t.coord] = out_region.piece(g, color)
+                    continue
                 with torch.cuda.stream(self.cstream(g)):
                     self.out_bufs[t.coord] = torch.zeros(t.out_rect.shape, dtype=torch.float64,
                                                          device=self.W.device(g))
@@ -384,6 +393,39 @@ class _Executor:
             self._sync(cur, self.xstream(g))
         self.buffers.clear()
         self.out_bufs.clear()
+
+    def _direct_commits(self, region) -> dict:
+        """Tasks whose leaves may write straight into their home piece.
+
+        Valid when the output region is a fresh +0.0 region, the task's only
+        commit targets a piece on its own GPU whose box is exactly the task's
+        output box, no other task commits into that piece, and the statement
+        does not read its own output.  Then "leaf into a zero buffer, then
+        canon (+)= buffer" and "leaf into canon" produce the same bits (the
+        reference's commit, `simulator.py:624-634`, adds to +0.0 exactly)."""
+        if not region.zeroed:
+            return {}
+        rhs = {a.tensor.name for leaf in leaf_statements(self.plan.task_body)
+               for a in accesses_of(leaf.rhs)}
+        if self.plan.out_name in rhs:
+            return {}
+        by_task, by_piece = {}, {}
+        for c in self.prog.commits:
+            by_task.setdefault(c.task.coord, []).append(c)
+            key = (self.gpu(c.home), c.color)
+            by_piece[key] = by_piece.get(key, 0) + 1
+        out = {}
+        for t in self.plan.tasks:
+            cs = by_task.get(t.coord, [])
+            if len(cs) != 1 or t.out_rect is None:
+                continue
+            c = cs[0]
+            g = self.gpu(t.coord)
+            if (self.gpu(c.home) == g and self.W.owns(g) and by_piece[(g, c.color)] == 1
+                    and c.part == t.out_rect == region.dist.piece_bounds(c.color)
+                    and (g, c.color) in region.pieces):
+                out[t.coord] = c.color
+        return out
 
     def transfers(self, moves):
         torch = self.torch
@@ -516,7 +558,7 @@ class _Executor:
         acc = plan.out_kind == "reduce"
         for k, c in enumerate(self.prog.commits):
             gh = self.gpu(c.home)
-            if not self.W.owns(gh):
+            if not self.W.owns(gh) or c.task.coord in self.direct:
                 continue
             piece = region.piece(gh, c.color)
             dst = _slice(piece, region.dist.piece_bounds(c.color), c.part)
@@ -543,6 +585,7 @@ def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: 
     _Executor(prog, store, leaf_policy).run()
     plan = prog.plan
     out_region = store[plan.out_name]
+    out_region.zeroed = False
     if plan.out_kind == "reduce" and out_region.dist.replicated:
         for color in out_region.dist.colors():
             procs = out_region.dist.processors_of(color)
