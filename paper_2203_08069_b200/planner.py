@@ -223,6 +223,8 @@ class Transfer:
     part: HyperRect
     src_hid: int
     dst_hid: int
+    wave: int = 0      # > 0: relays a temp received earlier in the same step
+
 
 
 @dataclass
@@ -330,6 +332,7 @@ def build_program(stmt, store, trace: ExecutionTrace, *, record_requirements=Tru
     for s in range(plan.num_steps):
         cur_temps: dict = {}
         moves: list = []
+        wave_of: dict = {}      # temp hid made this step -> wave of the transfer making it
         for task in plan.tasks:
             p = task.coord
             launch_iv = dict(plan.intervals)
@@ -369,7 +372,12 @@ def build_program(stmt, store, trace: ExecutionTrace, *, record_requirements=Tru
                                                     "copy", "compute"))
                             h = new_holding(proc=p, tensor=name, rect=part, kind="temp",
                                             step=s, scope=scope)
-                            moves.append(Transfer(s, src, p, name, part, src_hid, h.hid))
+                            # a source that is itself a temp received this step
+                            # (launch-scope relay, e.g. MTTKRP's D 00->01->10) must
+                            # be forwarded in a later NCCL group than its arrival
+                            wave = wave_of[src_hid] + 1 if src_hid in wave_of else 0
+                            wave_of[h.hid] = wave
+                            moves.append(Transfer(s, src, p, name, part, src_hid, h.hid, wave))
                             sink.setdefault(p, []).append(h.hid)
                             all_temps.setdefault(p, []).append(h.hid)
         for p in order:

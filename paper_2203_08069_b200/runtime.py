@@ -428,6 +428,13 @@ class _Executor:
         return out
 
     def transfers(self, moves):
+        """One NCCL group per relay wave (planner.Transfer.wave): a temp
+        forwarded in the step it arrives is sent only after its receive, by
+        stream order on the communication stream."""
+        for wave in sorted({t.wave for t in moves}):
+            self._transfer_group([t for t in moves if t.wave == wave])
+
+    def _transfer_group(self, moves):
         torch = self.torch
         sends, recvs = [], []
         for t in moves:
