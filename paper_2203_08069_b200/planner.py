@@ -275,7 +275,7 @@ def build_program(stmt, store, trace: ExecutionTrace, *, record_requirements=Tru
         return h
 
     # resident pieces of every tensor the launch touches
-    for name in {n for n, _, _ in plan.fetch_plan} | {plan.out_name}:
+    for name in sorted({n for n, _, _ in plan.fetch_plan} | {plan.out_name}):
         dist = store[name].dist
         held = store[name].residency
         for color, box, procs in dist.pieces():
@@ -515,3 +515,26 @@ def plan_statement(stmt, machine, distributions, schedule=None, *, record_requir
     trace.launches.append({"phase": "compute", "label": label or prog.plan.out_name,
                            "tasks": len(prog.plan.tasks), "steps": prog.plan.num_steps})
     return prog, trace
+
+
+def comm_schedule(prog: Program, machine, ngpus: int) -> list:
+    """Cross-GPU traffic of a program in issue order: one entry
+    (phase, step, wave, src_gpu, dst_gpu, elements) per NCCL send/recv pair.
+    Every SPMD rank derives the same list (planning is deterministic), takes
+    the sends and receives of its own GPU, and NCCL pairs them in this order;
+    same-GPU transfers are HBM aliases and do not appear."""
+    out = []
+    for s, moves in enumerate(prog.transfers):
+        for wave in sorted({t.wave for t in moves}):
+            for t in moves:
+                if t.wave != wave:
+                    continue
+                gs, gd = machine.device_of(t.src, ngpus), machine.device_of(t.dst, ngpus)
+                if gs != gd:
+                    out.append(("fetch", s, wave, gs, gd, t.part.volume))
+    last = prog.plan.num_steps - 1
+    for c in prog.commits:
+        gs, gd = machine.device_of(c.task.coord, ngpus), machine.device_of(c.home, ngpus)
+        if gs != gd:
+            out.append(("commit", last, 0, gs, gd, c.part.volume))
+    return out
