@@ -1,0 +1,36 @@
+# bench-size launches of each native leaf (one warm-up + one profiled), for ncu
+import ctypes as C, sys
+sys.path.insert(0, ".")
+import torch
+from paper_2203_08069_b200 import _native as nat
+nat.load()
+st = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)
+P = lambda t: C.c_void_p(t.data_ptr())
+def gen(shape, tid):
+    t = torch.empty(shape, dtype=torch.float64, device="cuda")
+    nat.call("td_generate", st(), len(shape), nat.i64_array(shape), nat.i64_array([0]*len(shape)), nat.i64_array(shape), P(t), nat.i64_array(t.stride()), 0, tid, 0)
+    return t
+which = sys.argv[1]
+if which == "gemm":
+    n = 16384
+    a, b = gen((n, n), 1), gen((n, n), 2); c = torch.empty(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2): nat.call("td_dgemm", st(), n, n, n, P(a), n, P(b), n, P(c), n, 0)
+elif which == "ttv":
+    n = 2048
+    b = gen((n, n, n), 1); cv = gen((n,), 2); a = torch.empty(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2): nat.call("td_ttv", st(), n, n, n, P(b), n*n, n, P(cv), P(a), n, 1, 0)
+elif which == "innerprod":
+    n = 2048
+    b = gen((n, n, n), 1); c2 = gen((n, n, n), 3)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda"); work = torch.empty(8192, dtype=torch.float64, device="cuda")
+    for _ in range(2): nat.call("td_innerprod", st(), 1, n**3, P(b), n**3, P(c2), n**3, P(out), P(work), 0)
+elif which == "ttm":
+    n, L = 1024, 64
+    b = gen((n, n, n), 1); cm = gen((n, L), 2); y = torch.empty(n, n, L, dtype=torch.float64, device="cuda")
+    for _ in range(2): nat.call("td_ttm", st(), n, n, n, L, P(b), n*n, n, P(cm), L, P(y), n*L, L, 0)
+elif which == "mttkrp":
+    n, R = 1024, 32
+    b = gen((n, n, n), 1); cm = gen((n, R), 2); d = gen((n, R), 3); a = torch.empty(n, R, dtype=torch.float64, device="cuda")
+    for _ in range(2): nat.call("td_mttkrp", st(), n, n, n, R, P(b), n*n, n, P(cm), R, P(d), R, P(a), R, 0)
+torch.cuda.synchronize()
+print("done", which)
