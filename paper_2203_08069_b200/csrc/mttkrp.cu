@@ -72,11 +72,35 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
   const int total = ltiles;
   const int64_t kbase = int64_t(kb) * ROWS;
 
+  // fixed-address fast path (full k-block, full l tile, full 32-wide j block)
+  constexpr int FB_PER_ROW = MK_BK / VEC, FD_PER_ROW = MK_R / VEC;
+  constexpr int FB_ITERS = ROWS * FB_PER_ROW / Cfg::THREADS, FB_STEP = Cfg::THREADS / FB_PER_ROW;
+  constexpr int FD_ITERS = MK_BK * FD_PER_ROW / Cfg::THREADS, FD_STEP = Cfg::THREADS / FD_PER_ROW;
+  static_assert(FB_ITERS * Cfg::THREADS == ROWS * FB_PER_ROW && FD_ITERS * Cfg::THREADS == MK_BK * FD_PER_ROW,
+                "mttkrp tile / thread mismatch");
+  const int fb_r = tid / FB_PER_ROW, fb_c = (tid % FB_PER_ROW) * VEC;
+  const int fd_r = tid / FD_PER_ROW, fd_c = (tid % FD_PER_ROW) * VEC;
+  const bool interior = kbase + ROWS <= K && j0 + MK_R <= R;
+  const double* fb_base = Bi + (kbase + fb_r) * p.sBk + fb_c;
+  const double* fd_base = p.D + int64_t(fd_r) * p.ldd + j0 + fd_c;
+  const int64_t fb_step = int64_t(FB_STEP) * p.sBk, fd_step = int64_t(FD_STEP) * p.ldd;
+
   auto load = [&](int stage, int t) {
     const int64_t k0 = kbase;
     const int64_t l0 = int64_t(t) * MK_BK;
     double* bs = Bs + stage * Cfg::A_STAGE;
     double* ds = Ds + stage * Cfg::D_STAGE;
+    if (interior && l0 + MK_BK <= L) {
+      const double* b = fb_base + l0;
+#pragma unroll
+      for (int it = 0; it < FB_ITERS; ++it)
+        cp_async_f64<VEC>(bs + (fb_r + it * FB_STEP) * MK_SA + fb_c, b + it * fb_step, VEC);
+      const double* d = fd_base + l0 * p.ldd;
+#pragma unroll
+      for (int it = 0; it < FD_ITERS; ++it)
+        cp_async_f64<VEC>(ds + (fd_r + it * FD_STEP) * MK_SD + fd_c, d + it * fd_step, VEC);
+      return;
+    }
     constexpr int B_PER_ROW = MK_BK / VEC;
 #pragma unroll 4
     for (int c = tid; c < ROWS * B_PER_ROW; c += Cfg::THREADS) {
