@@ -123,6 +123,12 @@ int td_nest_eval(void* stream, const void* prog, int64_t bytes);
 int td_copy_box(void* stream, int ndim, const int64_t* shape,
                 double* dst, const int64_t* dst_strides,
                 const double* src, const int64_t* src_strides, int accumulate);
+/* Pitched 2-D copy between host (pinned) and device or device and device:
+ * `rows` rows of `width` float64, row pitches in elements (cudaMemcpy2DAsync,
+ * direction inferred from the pointers).  Used to upload / download
+ * k-slabs of resident pieces while the leaves of earlier steps run. */
+int td_memcpy_2d(void* stream, double* dst, int64_t dst_pitch, const double* src, int64_t src_pitch,
+                 int64_t width, int64_t rows);
 /* fill a contiguous range with a constant */
 int td_fill(void* stream, double* dst, int64_t n, double value);
 /* Synthetic input generator: writes the box [origin, origin+shape) of a

@@ -41,6 +41,7 @@ _SIGNATURES = {
     "td_innerprod_work_size": ([], i64),
     "td_nest_eval": ([vp, vp, i64], i32),
     "td_copy_box": ([vp, i32, _I64P, dp, _I64P, dp, _I64P, i32], i32),
+    "td_memcpy_2d": ([vp, dp, i64, dp, i64, i64, i64], i32),
     "td_fill": ([vp, dp, i64, C.c_double], i32),
     "td_generate": ([vp, i32, _I64P, _I64P, _I64P, dp, _I64P, C.c_uint64, C.c_uint64, i32], i32),
     "td_nccl_version": ([], i32),

@@ -50,6 +50,14 @@ class World:
                                 torch.cuda.Stream(device=dev, priority=-1))
         return self._streams[g]
 
+    def copy_stream(self, g: int):
+        """Host<->device copy stream of an owned GPU (progressive placement)."""
+        key = ("h2d", g)
+        if key not in self._streams:
+            import torch
+            self._streams[key] = torch.cuda.Stream(device=self.torch_devices[g])
+        return self._streams[key]
+
     def comm(self, g: int):
         if g not in self.comms:
             raise ConfigError(f"GPU {g} has no NCCL communicator (job of {self.ngpus} GPU(s))")

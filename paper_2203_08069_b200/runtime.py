@@ -124,6 +124,7 @@ class RegionStore:
         self.machine = machine
         self.world = world or current_world()
         self.regions: dict = {}
+        self.ready: dict = {}     # (tensor, gpu, color) -> [(box, CUDA event)] of slabs still arriving
 
     def __contains__(self, name) -> bool:
         return name in self.regions
@@ -198,22 +199,55 @@ class RegionStore:
             if any(self.world.owns(g) for g in probe.gpus_of(color)):
                 yield color, box
 
-    def place_local(self, name: str, dist: TensorDistribution, host_pieces: dict) -> Region:
+    def place_local(self, name: str, dist: TensorDistribution, host_pieces: dict, *, slabs: int = 1,
+                    axis: int = 0) -> Region:
         """Upload per-piece host arrays (pinned for async H2D): host_pieces maps
         color -> array of that piece's box.  Only this process's pieces are
-        needed -- the e2e path of the benchmark."""
+        needed -- the e2e path of the benchmark.
+
+        With ``slabs > 1`` each piece arrives in that many slabs along `axis`
+        on the GPU's copy stream, each with its own event; `execute` makes a
+        leaf (or a send) wait only for the slabs its box touches, so the
+        upload of later k-slabs overlaps the leaves of earlier steps."""
         torch = torch_mod()
 
         def fill(g, color, box, buf):
-            st = self.world.streams(g)[0]
-            with torch.cuda.stream(st):
-                buf.copy_(torch.from_numpy(host_pieces[color]), non_blocking=True)
+            src = torch.from_numpy(host_pieces[color])
+            if slabs <= 1 or not box.lo:
+                st = self.world.streams(g)[0]
+                with torch.cuda.stream(st):
+                    buf.copy_(src, non_blocking=True)
+                buf.record_stream(st)
+                return
+            st = self.world.copy_stream(g)
+            n = box.shape[axis]
+            cuts = [(q * n) // slabs for q in range(slabs + 1)]
+            events = []
+            for a, b in zip(cuts, cuts[1:]):
+                if b <= a:
+                    continue
+                idx = tuple(slice(a, b) if d == axis else slice(None) for d in range(len(box.lo)))
+                _copy_any(st, buf[idx], src[idx])
+                ev = torch.cuda.Event()
+                ev.record(st)
+                lo = list(box.lo)
+                hi = list(box.hi)
+                lo[axis], hi[axis] = box.lo[axis] + a, box.lo[axis] + b
+                events.append((HyperRect(lo, hi), ev))
             buf.record_stream(st)
+            self.ready[(name, g, color)] = events
 
         region = self._alloc(name, dist, fill)
-        for g in self.world.owned:
-            torch.cuda.current_stream(self.world.device(g)).wait_stream(self.world.streams(g)[0])
+        if slabs <= 1:
+            for g in self.world.owned:
+                torch.cuda.current_stream(self.world.device(g)).wait_stream(self.world.streams(g)[0])
         return region
+
+    def wait_ready(self, stream, name, g, color, rect) -> None:
+        """Make `stream` wait for the slabs of piece (name, g, color) that `rect` touches."""
+        for box, ev in self.ready.get((name, g, color), ()):
+            if not rect.lo or box.intersect(rect) is not None:
+                stream.wait_event(ev)
 
     def zero(self, name: str) -> None:
         """Reset every resident piece of a region to +0.0 (a fresh output)."""
@@ -277,10 +311,48 @@ def _torch_current(buf):
 
 
 def _h2d_box(stream, dst, src):
-    """Host (strided) -> device box copy, one cudaMemcpyAsync per contiguous row run."""
-    import torch
-    tmp = src.contiguous()
-    dst.copy_(tmp, non_blocking=False)
+    """Host (strided) -> device box copy."""
+    _copy_any(stream, dst, src)
+
+
+def _copy_any(stream, dst, src):
+    """Async copy between two same-shape views (host pinned <-> device or
+    device <-> device) with pitched 2-D DMA copies: the views' trailing axes
+    must be unit-stride; leading axes are collapsed when possible and looped
+    otherwise."""
+    shape = tuple(dst.shape)
+    if not shape:
+        dst.copy_(src, non_blocking=True)
+        return
+    if dst.is_contiguous() and src.is_contiguous():
+        n = dst.numel()
+        _native.call("td_memcpy_2d", stream_handle(stream), C.c_void_p(dst.data_ptr()), n,
+                     C.c_void_p(src.data_ptr()), n, n, 1)
+        return
+    if dst.stride()[-1] != 1 or src.stride()[-1] != 1:
+        raise ConfigError("pitched copies need unit-stride rows")
+    if len(shape) == 1:
+        _native.call("td_memcpy_2d", stream_handle(stream), C.c_void_p(dst.data_ptr()), shape[0],
+                     C.c_void_p(src.data_ptr()), shape[0], shape[0], 1)
+        return
+    # collapse leading axes that are uniformly strided on both sides
+    def rows_of(t):
+        st, sh = t.stride(), t.shape
+        pitch = st[-2]
+        for d in range(len(sh) - 2, 0, -1):
+            if st[d - 1] != st[d] * sh[d]:
+                return None
+        return pitch
+    pd, ps = rows_of(dst), rows_of(src)
+    if pd is not None and ps is not None:
+        rows = 1
+        for e in shape[:-1]:
+            rows *= e
+        _native.call("td_memcpy_2d", stream_handle(stream), C.c_void_p(dst.data_ptr()), pd,
+                     C.c_void_p(src.data_ptr()), ps, shape[-1], rows)
+        return
+    for q in range(shape[0]):
+        _copy_any(stream, dst[q], src[q])
 
 
 def _bcast_piece(W, root_g, box, arr):
@@ -330,6 +402,7 @@ class _Executor:
         self.policy = policy
         self.m = store.machine
         self.buffers = {}            # hid -> CUDA tensor (owned GPUs only)
+        self.alias_origin = {}       # temp hid aliasing a piece -> (tensor, gpu, color)
         self.out_bufs = {}           # task coord -> CUDA tensor of out_rect
         self.torch = torch_mod()
         self.gpus = sorted({self.gpu(t.coord) for t in self.plan.tasks} |
@@ -351,6 +424,19 @@ class _Executor:
         if h.kind == "piece":
             return self.store[h.tensor].piece(self.gpu(h.proc), h.color)
         return self.buffers[hid]
+
+    def origin(self, hid):
+        """(tensor, gpu, color) of the resident piece a holding views, if any."""
+        h = self.prog.holdings[hid]
+        if h.kind == "piece":
+            return (h.tensor, self.gpu(h.proc), h.color)
+        return self.alias_origin.get(hid)
+
+    def wait_piece(self, stream, hid, rect):
+        """Progressive placement: wait for the slabs of the underlying piece."""
+        o = self.origin(hid)
+        if o is not None and self.store.ready:
+            self.store.wait_ready(stream, o[0], o[1], o[2], rect)
 
     def _sync(self, waiter, producer):
         ev = self.torch.cuda.Event()
@@ -443,9 +529,13 @@ class _Executor:
                 if self.W.owns(gs):
                     src_h = self.prog.holdings[t.src_hid]
                     self.buffers[t.dst_hid] = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
+                    o = self.origin(t.src_hid)
+                    if o is not None:
+                        self.alias_origin[t.dst_hid] = o
                 continue
             if self.W.owns(gs):
                 src_h = self.prog.holdings[t.src_hid]
+                self.wait_piece(self.xstream(gs), t.src_hid, t.part)
                 view = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
                 if not view.is_contiguous():
                     st = self.xstream(gs)
@@ -480,10 +570,12 @@ class _Executor:
     def operand(self, g, name, rect, hids):
         """A CUDA view holding `rect` of tensor `name` on GPU g."""
         torch = self.torch
+        st = self.cstream(g)
+        for hid in hids:
+            self.wait_piece(st, hid, rect)
         if len(hids) == 1 and self.prog.holdings[hids[0]].rect.contains(rect):
             h = self.prog.holdings[hids[0]]
             return _slice(self.holding_buf(hids[0]), h.rect, rect)
-        st = self.cstream(g)
         with torch.cuda.stream(st):
             buf = torch.zeros(rect.shape, dtype=torch.float64, device=self.W.device(g))
         for hid in hids:
