@@ -377,6 +377,22 @@ def bench_kernels(job, steps, warmup):
         gc.collect()
         torch.cuda.empty_cache()
 
+    # G1: SUMMA 1024^3 on a 2x2 grid, chunk 128 (the reference's results-oracle config;
+    # fixed size, latency-bound: 4 tasks x 8 steps of 512x512x128 DMMA leaves)
+    g1 = td.summa(2, 2, dims=(1024, 1024, 1024), chunk=128)
+    cin, store = g1.prepare(seed=0, mode=0, world=job.world)
+
+    def g1_step():
+        store.zero("C")
+        td.execute(cin, store, record_requirements=False)
+
+    ms = job.timed(g1_step, 20, 5)
+    results["summa_1024_2x2"] = {"config": "summa 2x2 dims (1024, 1024, 1024) chunk 128", "value":
+                                 2.0 * 1024 ** 3 * 20 / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
+                                 "ms_per_step": ms / 20, "scaling": "strong (fixed size)"}
+    del store, g1_step
+    gc.collect()
+
     n = 2048
     run("ttv_2048", td.ttv(p, dims=(n * p, n, n)), 8.0 * (n ** 3 + n + n * n) * p, "GB/s", hbm, "ttv")
     run("innerprod3_2048", td.innerprod3(p, dims=(n * p, n, n)), 16.0 * n ** 3 * p, "GB/s", hbm, "innerprod")

@@ -2,22 +2,19 @@
 // (reference statement pkg/src/tendist/algorithms.py:339-340, evaluated per
 // point at cin.py:399-417 in the reference).
 //
-// One CTA owns one i (and one 32-wide block of j):
-//   for each k-block of ROWS = 32*WARPS rows:
-//        T[ROWS x 32] = B(i, kblk, :) . D[:, jblk] on DMMA.8x8x4 tiles (every
-//        warp 32 x 32, 16 DMMA per k4 slice) fed by a cp.async ring over l
-//        (16 per stage);
-//   epilogue per k-block: partial(j) += sum_k C(k,j) * T(k,j) in registers;
-//   end: fixed-order shuffle + shared-memory tree over the warps.
-// The (i, k-block) pairs are independent CTAs (I x ceil(K/ROWS) of them, so
-// the grid is many waves deep and the tail is small); each writes its partial
-// row to a stream-ordered workspace and a second kernel sums the k-blocks of
-// every A(i, :) in ascending order and writes (or accumulates) A.
-// No atomics: the summation order is a fixed function of the shape, so runs
-// are bitwise reproducible; exact on integer-valued data.
+// A CTA owns one i, one 32-wide block of j and KPC consecutive k-blocks of
+// ROWS = 32*WARPS rows.  For each k-block:
+//     T[ROWS x 32] = B(i, kblk, :) . D[:, jblk]  on DMMA.8x8x4 tiles (every
+//     warp 32 x 32, 16 DMMA per k4 slice) fed by one cp.async ring over
+//     (k-block, l-tile) pairs, so the pipeline never drains between k-blocks;
+//     epilogue: partial(j) += sum_k C(k,j) * T(k,j) in registers.
+// At the end a fixed-order shuffle + shared-memory tree reduces the partial
+// over the warps and the CTA writes it to a stream-ordered workspace
+// [I][groups][R]; `mttkrp_reduce` then sums the groups of every A(i, :) in
+// ascending order and writes (or accumulates) A.  No atomics: the summation
+// order is a fixed function of the shape, runs are bitwise reproducible, and
+// integer-valued inputs give exact results.
 // B is streamed once from HBM (8 B per 64 flop at R = 32); D and C stay in L2.
-// Small CTAs (4 warps, ~75-100 KB smem) let 2-3 of them share an SM, so one
-// CTA's barrier / epilogue is covered by another's DMMA issue.
 #include "common.cuh"
 #include "dmma.cuh"
 
@@ -25,7 +22,7 @@ namespace td {
 
 constexpr int MK_BK = 16;              // l per pipeline stage
 constexpr int MK_R = 32;               // j columns per CTA
-constexpr int MK_SA = MK_BK + 4;       // B-tile row stride (doubles)
+constexpr int MK_SA = MK_BK + 4;       // B-tile row stride (doubles): conflict-free fragments
 constexpr int MK_SD = MK_R + 4;        // D-tile row stride
 
 template <int WARPS, int STAGES>
@@ -48,10 +45,11 @@ struct MttkrpArgs {
   double* A;
   int64_t lda;
   int accumulate;
-  double* work;   // [I][kblocks][R] partials
+  double* work;   // [I][groups][R] partials
+  int kblocks, groups;
 };
 
-template <int WARPS, int STAGES, int VEC>
+template <int WARPS, int STAGES, int KPC, int VEC>
 __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(MttkrpArgs p) {
   using Cfg = MkCfg<WARPS, STAGES>;
   constexpr int ROWS = Cfg::ROWS;
@@ -60,17 +58,16 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
   double* Ds = smem + STAGES * Cfg::A_STAGE;
   double* red = Ds + STAGES * Cfg::D_STAGE;  // [WARPS][32]
 
-  const int kblocks = (int)ceil_div(p.K, ROWS);
-  const int64_t i = blockIdx.x / kblocks;
-  const int kb = blockIdx.x % kblocks;
+  const int64_t i = blockIdx.x / p.groups;
+  const int grp = blockIdx.x % p.groups;
+  const int kb0 = grp * KPC;
+  const int nkb = min(KPC, p.kblocks - kb0);
   const int64_t j0 = int64_t(blockIdx.y) * MK_R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* __restrict__ Bi = p.B + i * p.sBi;
   const int64_t K = p.K, L = p.L, R = p.R;
-
   const int ltiles = (int)ceil_div(L, MK_BK);
-  const int total = ltiles;
-  const int64_t kbase = int64_t(kb) * ROWS;
+  const int total = nkb * ltiles;
 
   // fixed-address fast path (full k-block, full l tile, full 32-wide j block)
   constexpr int FB_PER_ROW = MK_BK / VEC, FD_PER_ROW = MK_R / VEC;
@@ -80,18 +77,17 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
                 "mttkrp tile / thread mismatch");
   const int fb_r = tid / FB_PER_ROW, fb_c = (tid % FB_PER_ROW) * VEC;
   const int fd_r = tid / FD_PER_ROW, fd_c = (tid % FD_PER_ROW) * VEC;
-  const bool interior = kbase + ROWS <= K && j0 + MK_R <= R;
-  const double* fb_base = Bi + (kbase + fb_r) * p.sBk + fb_c;
+  const bool jfull = j0 + MK_R <= R;
   const double* fd_base = p.D + int64_t(fd_r) * p.ldd + j0 + fd_c;
   const int64_t fb_step = int64_t(FB_STEP) * p.sBk, fd_step = int64_t(FD_STEP) * p.ldd;
 
   auto load = [&](int stage, int t) {
-    const int64_t k0 = kbase;
-    const int64_t l0 = int64_t(t) * MK_BK;
+    const int64_t k0 = int64_t(kb0 + t / ltiles) * ROWS;
+    const int64_t l0 = int64_t(t % ltiles) * MK_BK;
     double* bs = Bs + stage * Cfg::A_STAGE;
     double* ds = Ds + stage * Cfg::D_STAGE;
-    if (interior && l0 + MK_BK <= L) {
-      const double* b = fb_base + l0;
+    if (jfull && k0 + ROWS <= K && l0 + MK_BK <= L) {
+      const double* b = Bi + (k0 + fb_r) * p.sBk + fb_c + l0;
 #pragma unroll
       for (int it = 0; it < FB_ITERS; ++it)
         cp_async_f64<VEC>(bs + (fb_r + it * FB_STEP) * MK_SA + fb_c, b + it * fb_step, VEC);
@@ -169,8 +165,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
 #pragma unroll
         for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
     }
-    if (t == total - 1) {  // k-block finished: Hadamard with C, reduce over k
-      const int64_t k0 = kbase;
+    if (t % ltiles == ltiles - 1) {  // k-block finished: Hadamard with C, reduce over its k rows
+      const int64_t k0 = int64_t(kb0 + t / ltiles) * ROWS;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const int64_t k = k0 + warp * 32 + m * 8 + (lane >> 2);
@@ -213,18 +209,18 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) v += red[w * MK_R + tid];
     const int64_t j = j0 + tid;
-    if (j < R) p.work[(i * kblocks + kb) * R + j] = v;
+    if (j < R) p.work[(i * p.groups + grp) * R + j] = v;
   }
 }
 
-// A(i, j) (+)= sum over k-blocks, ascending (fixed order)
-__global__ void mttkrp_reduce(const double* __restrict__ work, int kblocks, int64_t I, int64_t R, double* A,
+// A(i, j) (+)= sum over the CTA groups of row i, ascending (fixed order)
+__global__ void mttkrp_reduce(const double* __restrict__ work, int groups, int64_t I, int64_t R, double* A,
                               int64_t lda, int accumulate) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < I * R; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / R, j = e - (e / R) * R;
-    const double* w = work + i * kblocks * R + j;
+    const double* w = work + i * groups * R + j;
     double v = 0.0;
-    for (int kb = 0; kb < kblocks; ++kb) v += w[int64_t(kb) * R];
+    for (int g = 0; g < groups; ++g) v += w[int64_t(g) * R];
     double* dst = A + i * lda + j;
     *dst = accumulate ? *dst + v : v;
   }
@@ -232,44 +228,46 @@ __global__ void mttkrp_reduce(const double* __restrict__ work, int kblocks, int6
 
 static bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
 
-template <int WARPS, int STAGES>
+static int retain_pool() {  // keep the stream-ordered pool's memory across syncs
+  int dev = 0;
+  TD_CUDA(cudaGetDevice(&dev));
+  static bool retained[64] = {false};
+  if (dev < 64 && !retained[dev]) {
+    cudaMemPool_t pool;
+    TD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    TD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    retained[dev] = true;
+  }
+  return TD_OK;
+}
+
+template <int WARPS, int STAGES, int KPC>
 static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
   using Cfg = MkCfg<WARPS, STAGES>;
-  const int64_t kblocks = std::max<int64_t>(1, ceil_div(a.K, Cfg::ROWS));
-  TD_REQUIRE(a.I * kblocks < (1ll << 31), "mttkrp: grid too large");
-  {  // keep the stream-ordered pool's memory across syncs (no re-mapping per call)
-    int dev = 0;
-    TD_CUDA(cudaGetDevice(&dev));
-    static bool retained[64] = {false};
-    if (dev < 64 && !retained[dev]) {
-      cudaMemPool_t pool;
-      TD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-      uint64_t keep = ~0ull;
-      TD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-      retained[dev] = true;
-    }
-  }
-  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * kblocks * a.R, st));
-  if (a.K <= 0) {
-    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.R, st));
-  }
-  dim3 grid((unsigned)(a.K > 0 ? a.I * kblocks : 0), (unsigned)ceil_div(a.R, MK_R));
+  a.kblocks = (int)std::max<int64_t>(1, ceil_div(a.K, Cfg::ROWS));
+  a.groups = (int)ceil_div(a.kblocks, KPC);
+  TD_REQUIRE(a.I * a.groups < (1ll << 31), "mttkrp: grid too large");
+  if (int rc = retain_pool()) return rc;
+  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * a.groups * a.R, st));
   if (a.K > 0) {
-  if (vec2) {
-    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
-    mttkrp_kernel<WARPS, STAGES, 2><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+    dim3 grid((unsigned)(a.I * a.groups), (unsigned)ceil_div(a.R, MK_R));
+    if (vec2) {
+      TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, KPC, 2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      mttkrp_kernel<WARPS, STAGES, KPC, 2><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+    } else {
+      TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, KPC, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      mttkrp_kernel<WARPS, STAGES, KPC, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+    }
+    if (int rc = check_launch("mttkrp_kernel")) return rc;
   } else {
-    TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
-    mttkrp_kernel<WARPS, STAGES, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
-  }
-  int rc = check_launch("mttkrp_kernel");
-  if (rc) return rc;
+    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.groups * a.R, st));
   }
   const int64_t outs = a.I * a.R;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(outs, 256), 148 * 8));
-  mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, (int)kblocks, a.I, a.R, a.A, a.lda, a.accumulate);
+  mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, a.groups, a.I, a.R, a.A, a.lda, a.accumulate);
   int rc = check_launch("mttkrp_reduce");
   TD_CUDA(cudaFreeAsync(a.work, st));
   return rc;
@@ -278,10 +276,13 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
 int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
   switch (config < 0 ? 1 : config) {
-    case 0: return launch_mttkrp<4, 4>(st, a, vec2);
-    case 1: return launch_mttkrp<4, 3>(st, a, vec2);
-    case 2: return launch_mttkrp<8, 3>(st, a, vec2);
-    case 3: return launch_mttkrp<2, 4>(st, a, vec2);
+    case 0: return launch_mttkrp<4, 4, 1>(st, a, vec2);
+    case 1: return launch_mttkrp<4, 3, 1>(st, a, vec2);
+    case 2: return launch_mttkrp<4, 3, 2>(st, a, vec2);
+    case 3: return launch_mttkrp<4, 3, 4>(st, a, vec2);
+    case 4: return launch_mttkrp<4, 4, 2>(st, a, vec2);
+    case 5: return launch_mttkrp<2, 4, 2>(st, a, vec2);
+    case 6: return launch_mttkrp<4, 3, 8>(st, a, vec2);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;
@@ -296,7 +297,7 @@ extern "C" int td_mttkrp_config(void* stream, int config, int64_t I, int64_t K, 
   using namespace td;
   if (I <= 0 || R <= 0) return TD_OK;
   TD_REQUIRE(I <= 2147483647, "mttkrp: I too large");
-  MttkrpArgs a{I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate, nullptr};
+  MttkrpArgs a{I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate, nullptr, 0, 0};
   return mttkrp_dispatch(as_stream(stream), a, config);
 }
 

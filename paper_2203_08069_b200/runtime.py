@@ -495,11 +495,10 @@ class _Executor:
                for a in accesses_of(leaf.rhs)}
         if self.plan.out_name in rhs:
             return {}
-        by_task, by_piece = {}, {}
+        by_task, first = {}, {}
         for c in self.prog.commits:
             by_task.setdefault(c.task.coord, []).append(c)
-            key = (self.gpu(c.home), c.color)
-            by_piece[key] = by_piece.get(key, 0) + 1
+            first.setdefault((self.gpu(c.home), c.color), c)
         out = {}
         for t in self.plan.tasks:
             cs = by_task.get(t.coord, [])
@@ -507,7 +506,9 @@ class _Executor:
                 continue
             c = cs[0]
             g = self.gpu(t.coord)
-            if (self.gpu(c.home) == g and self.W.owns(g) and by_piece[(g, c.color)] == 1
+            # the first committer of a zeroed piece may write it in place: later
+            # reductions (Johnson's depth partials) still add in task order
+            if (self.gpu(c.home) == g and self.W.owns(g) and first[(g, c.color)] is c
                     and c.part == t.out_rect == region.dist.piece_bounds(c.color)
                     and (g, c.color) in region.pieces):
                 out[t.coord] = c.color
