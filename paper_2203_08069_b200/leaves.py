@@ -318,15 +318,41 @@ def _timing_stop(kind, ev, stream):
     TIMING.append((kind, ev, end))
 
 
+_MEMO: dict = {}
+
+
+def _classify_cached(leaf):
+    hit = _MEMO.get(("cls", id(leaf)))
+    if hit is not None and hit[0] is leaf:
+        return hit[1]
+    m = classify(leaf)
+    _MEMO[("cls", id(leaf))] = (leaf, m)
+    return m
+
+
+def _box_cached(loops, leaf, defs):
+    """box_of memoised on (nest bounds, leaf, relation map): the bounds of a
+    task's step nest repeat across steps and across repeated executes."""
+    key = ("box", tuple(loops), id(leaf), id(defs))
+    hit = _MEMO.get(key)
+    if hit is not None and hit[0] is leaf and hit[1] is defs:
+        return hit[2]
+    if len(_MEMO) > 65536:
+        _MEMO.clear()
+    box = box_of(loops, leaf, defs)
+    _MEMO[key] = (leaf, defs, box)
+    return box
+
+
 def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream) -> str:
     """Execute one step nest; returns the path taken ("dgemm", ..., "nest").
 
     policy: "auto" | a builtin contraction name | "interpreter" / "exact"."""
     if isinstance(leaf, Reduce) and policy not in ("interpreter", "exact"):
-        m = classify(leaf)
+        m = _classify_cached(leaf)
         want = {"gemm": "dgemm"}.get(policy, policy)
         if m is not None and (want == "auto" or want == m.kind):
-            box = box_of(loops, leaf, defs)
+            box = _box_cached(loops, leaf, defs)
             if box == {}:
                 return "empty"
             if box is not None:
