@@ -50,9 +50,10 @@ class World:
                                 torch.cuda.Stream(device=dev, priority=-1))
         return self._streams[g]
 
-    def copy_stream(self, g: int):
-        """Host<->device copy stream of an owned GPU (progressive placement)."""
-        key = ("h2d", g)
+    def copy_stream(self, g: int, k: int = 0):
+        """Host<->device copy stream k of an owned GPU (progressive placement;
+        independent streams let several inputs upload concurrently)."""
+        key = ("h2d", g, k)
         if key not in self._streams:
             import torch
             self._streams[key] = torch.cuda.Stream(device=self.torch_devices[g])

@@ -125,6 +125,8 @@ class RegionStore:
         self.world = world or current_world()
         self.regions: dict = {}
         self.ready: dict = {}     # (tensor, gpu, color) -> [(box, CUDA event)] of slabs still arriving
+        self.done: dict = {}      # (tensor, gpu, color) -> CUDA event after the last write of a launch
+        self.pending: dict = {}   # (tensor, gpu, color) -> [box, buf, host, slabs left] deferred uploads
 
     def __contains__(self, name) -> bool:
         return name in self.regions
@@ -200,7 +202,7 @@ class RegionStore:
                 yield color, box
 
     def place_local(self, name: str, dist: TensorDistribution, host_pieces: dict, *, slabs: int = 1,
-                    axis: int = 0) -> Region:
+                    axis: int = 0, copy_stream: int = 0, defer: bool = False) -> Region:
         """Upload per-piece host arrays (pinned for async H2D): host_pieces maps
         color -> array of that piece's box.  Only this process's pieces are
         needed -- the e2e path of the benchmark.
@@ -208,43 +210,70 @@ class RegionStore:
         With ``slabs > 1`` each piece arrives in that many slabs along `axis`
         on the GPU's copy stream, each with its own event; `execute` makes a
         leaf (or a send) wait only for the slabs its box touches, so the
-        upload of later k-slabs overlaps the leaves of earlier steps."""
+        upload of later k-slabs overlaps the leaves of earlier steps.  With
+        ``defer=True`` only the buffers are allocated and the caller orders
+        the copies itself with `upload` (all before `execute`)."""
         torch = torch_mod()
 
         def fill(g, color, box, buf):
             src = torch.from_numpy(host_pieces[color])
-            if slabs <= 1 or not box.lo:
+            if defer:
+                self.pending[(name, g, color)] = [box, buf, src, None]
+            elif slabs <= 1 or not box.lo:
                 st = self.world.streams(g)[0]
                 with torch.cuda.stream(st):
                     buf.copy_(src, non_blocking=True)
                 buf.record_stream(st)
-                return
-            st = self.world.copy_stream(g)
-            n = box.shape[axis]
-            cuts = [(q * n) // slabs for q in range(slabs + 1)]
-            events = []
-            for a, b in zip(cuts, cuts[1:]):
-                if b <= a:
-                    continue
-                idx = tuple(slice(a, b) if d == axis else slice(None) for d in range(len(box.lo)))
-                _copy_any(st, buf[idx], src[idx])
-                ev = torch.cuda.Event()
-                ev.record(st)
-                lo = list(box.lo)
-                hi = list(box.hi)
-                lo[axis], hi[axis] = box.lo[axis] + a, box.lo[axis] + b
-                events.append((HyperRect(lo, hi), ev))
-            buf.record_stream(st)
-            self.ready[(name, g, color)] = events
+            else:
+                self.pending[(name, g, color)] = [box, buf, src, None]
+                self.upload(name, color, slabs=slabs, axis=axis, copy_stream=copy_stream)
 
         region = self._alloc(name, dist, fill)
-        if slabs <= 1:
+        if slabs <= 1 and not defer:
             for g in self.world.owned:
                 torch.cuda.current_stream(self.world.device(g)).wait_stream(self.world.streams(g)[0])
         return region
 
+    def upload(self, name: str, color, *, slabs: int = 1, axis: int = 0, copy_stream: int = 0,
+               only=None) -> None:
+        """Enqueue the H2D copy of (some slabs of) a deferred piece on every
+        owned GPU holding it; `only` selects slab indices (default: all)."""
+        torch = torch_mod()
+        for (n, g, c), rec in list(self.pending.items()):
+            if n != name or c != color:
+                continue
+            box, buf, src, left = rec
+            if left is None:
+                left = rec[3] = set(range(slabs))
+            st = self.world.copy_stream(g, copy_stream)
+            size = box.shape[axis] if box.lo else 1
+            cuts = [(q * size) // slabs for q in range(slabs + 1)]
+            events = self.ready.setdefault((name, g, color), [])
+            for q in sorted(left if only is None else set(only) & left):
+                a, b = cuts[q], cuts[q + 1]
+                left.discard(q)
+                if b <= a:
+                    continue
+                if box.lo:
+                    idx = tuple(slice(a, b) if d == axis else slice(None) for d in range(len(box.lo)))
+                    _copy_any(st, buf[idx], src[idx])
+                    lo, hi = list(box.lo), list(box.hi)
+                    lo[axis], hi[axis] = box.lo[axis] + a, box.lo[axis] + b
+                    part = HyperRect(lo, hi)
+                else:
+                    _copy_any(st, buf, src)
+                    part = box
+                ev = torch.cuda.Event()
+                ev.record(st)
+                events.append((part, ev))
+            buf.record_stream(st)
+            if not left:
+                del self.pending[(n, g, c)]
+
     def wait_ready(self, stream, name, g, color, rect) -> None:
         """Make `stream` wait for the slabs of piece (name, g, color) that `rect` touches."""
+        if (name, g, color) in self.pending:
+            raise ConfigError(f"{name} piece {color} still has slabs that were never uploaded")
         for box, ev in self.ready.get((name, g, color), ()):
             if not rect.lo or box.intersect(rect) is not None:
                 stream.wait_event(ev)
@@ -435,7 +464,7 @@ class _Executor:
     def wait_piece(self, stream, hid, rect):
         """Progressive placement: wait for the slabs of the underlying piece."""
         o = self.origin(hid)
-        if o is not None and self.store.ready:
+        if o is not None and (self.store.ready or self.store.pending):
             self.store.wait_ready(stream, o[0], o[1], o[2], rect)
 
     def _sync(self, waiter, producer):
@@ -463,22 +492,85 @@ class _Executor:
                     self.out_bufs[t.coord] = torch.zeros(t.out_rect.shape, dtype=torch.float64,
                                                          device=self.W.device(g))
         nsteps = self.plan.num_steps
-        for s in range(nsteps):
-            self.transfers(self.prog.transfers[s])
-            for g in self.owned:
-                self._sync(self.cstream(g), self.xstream(g))
-            if self.prog.stepwise:
-                self.compute(self.prog.work[s], s)
-            self.release(s)
-        if not self.prog.stepwise:
-            self.compute(self.prog.work[-1], -1)
-        self.commit(out_region)
+        if self._local_only():
+            self._run_task_major(out_region)
+        else:
+            for s in range(nsteps):
+                self.transfers(self.prog.transfers[s])
+                for g in self.owned:
+                    self._sync(self.cstream(g), self.xstream(g))
+                if self.prog.stepwise:
+                    self.compute(self.prog.work[s], s)
+                self.release(s)
+            if not self.prog.stepwise:
+                self.compute(self.prog.work[-1], -1)
+            self.commit(out_region)
+            self._mark_done(out_region, self.prog.commits)
         for g in self.owned:
             cur = torch.cuda.current_stream(self.W.device(g))
             self._sync(cur, self.cstream(g))
             self._sync(cur, self.xstream(g))
         self.buffers.clear()
         self.out_bufs.clear()
+
+    def _local_only(self) -> bool:
+        """No transfer or commit crosses GPUs (e.g. every single-GPU run)."""
+        if not self.prog.stepwise:
+            return False
+        for moves in self.prog.transfers:
+            for t in moves:
+                if self.gpu(t.src) != self.gpu(t.dst):
+                    return False
+        return all(self.gpu(c.task.coord) == self.gpu(c.home) for c in self.prog.commits)
+
+    def _run_task_major(self, region):
+        """Task-major order for GPU-local programs: each task runs all its
+        steps and commits before the next task starts.  Every transfer is an
+        HBM alias, each task's step order and the task-order commits are
+        unchanged, so results are identical to the step-major order -- but a
+        task's output pieces are final early, and `store.done` events let a
+        caller start their download while later tasks still compute."""
+        for s, moves in enumerate(self.prog.transfers):
+            self.transfers(moves)
+        by_task = {}
+        for s, works in enumerate(self.prog.work):
+            for w in works:
+                by_task.setdefault(w.task.coord, []).append((s, w))
+        commits = {}
+        for c in self.prog.commits:
+            commits.setdefault(c.task.coord, []).append(c)
+        for task in self.plan.tasks:
+            for s, w in by_task.get(task.coord, []):
+                self.compute([w], s)
+            mine = commits.get(task.coord, [])
+            self._apply_commits(region, [(c, None) for c in mine])
+            self._mark_done(region, mine, upto=task.coord)
+
+    def _mark_done(self, region, commits, upto=None):
+        """Record, per output piece, an event after its last commit."""
+        last = {}
+        for c in self.prog.commits:
+            last[(self.gpu(c.home), c.color)] = c.task.coord
+        for c in commits:
+            key = (self.gpu(c.home), c.color)
+            if not self.W.owns(key[0]) or (upto is not None and last[key] != upto):
+                continue
+            ev = self.torch.cuda.Event()
+            ev.record(self.cstream(key[0]))
+            self.store.done[(self.plan.out_name,) + key] = ev
+
+    def _apply_commits(self, region, items):
+        """Apply (commit, staged buffer or None) in order on the home GPUs."""
+        acc = self.plan.out_kind == "reduce"
+        for c, staged in items:
+            gh = self.gpu(c.home)
+            if not self.W.owns(gh) or c.task.coord in self.direct:
+                continue
+            piece = region.piece(gh, c.color)
+            dst = _slice(piece, region.dist.piece_bounds(c.color), c.part)
+            src = staged if staged is not None else _slice(self.out_bufs[c.task.coord], c.task.out_rect,
+                                                           c.part)
+            _copy_box(self.cstream(gh), dst, src, accumulate=acc)
 
     def _direct_commits(self, region) -> dict:
         """Tasks whose leaves may write straight into their home piece.
@@ -655,27 +747,22 @@ class _Executor:
         self._nccl(sends, recvs)
         for g in self.owned:
             self._sync(self.cstream(g), self.xstream(g))
-        acc = plan.out_kind == "reduce"
-        for k, c in enumerate(self.prog.commits):
-            gh = self.gpu(c.home)
-            if not self.W.owns(gh) or c.task.coord in self.direct:
-                continue
-            piece = region.piece(gh, c.color)
-            dst = _slice(piece, region.dist.piece_bounds(c.color), c.part)
-            if k in staged:
-                src = staged[k]
-            else:
-                src = _slice(self.out_bufs[c.task.coord], c.task.out_rect, c.part)
-            _copy_box(self.cstream(gh), dst, src, accumulate=acc)
+        self._apply_commits(region, [(c, staged.get(k)) for k, c in enumerate(self.prog.commits)])
+
+
+_PLAN_CACHE: dict = {}
 
 
 def _plan_cached(stmt, store, trace, record_requirements):
     """build_program, memoised per (statement object, store layout): repeated
     executes of one scheduled statement on one store (benchmark steps,
     iterative solvers) skip the Python planning and replay its ledger."""
-    layout = tuple((n, id(r.dist), tuple(len(v) for v in r.residency.values()))
-                   for n, r in sorted(store.regions.items()))
-    cache = store.__dict__.setdefault("_plan_cache", {})
+    # the program depends on the distributions and residency only, not on the
+    # store object or its values: key on those so fresh stores (e2e steps) hit
+    layout = (store.machine, store.world.ngpus,
+              tuple((n, r.dist, tuple(len(v) for v in r.residency.values()))
+                    for n, r in sorted(store.regions.items())))
+    cache = _PLAN_CACHE
     key = (id(stmt), bool(record_requirements))
     hit = cache.get(key)
     if hit is not None and hit[0] is stmt and hit[1] == layout:
@@ -691,6 +778,8 @@ def _plan_cached(stmt, store, trace, record_requirements):
     trace.requirements.extend(scratch.requirements)
     for p, v in scratch.memory.items():
         trace.bump_memory(p, v)
+    if len(cache) > 256:
+        cache.clear()
     cache[key] = (stmt, layout, prog, list(scratch.events), list(scratch.requirements), dict(scratch.memory))
     return prog
 

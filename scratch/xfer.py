@@ -1,0 +1,17 @@
+import torch, time
+n = 1 << 28  # 2 GiB of fp64
+h = torch.empty(n, dtype=torch.float64, pin_memory=True); h.fill_(1.0)
+d = torch.empty(n, dtype=torch.float64, device="cuda")
+for name, fn in [("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))]:
+    fn(); torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    s.record(); fn(); e.record(); e.synchronize()
+    print(name, 8 * n / s.elapsed_time(e) / 1e6, "GB/s")
+# concurrent h2d + d2h on two streams
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+h2 = torch.empty(n, dtype=torch.float64, pin_memory=True); d2 = torch.empty(n, dtype=torch.float64, device="cuda")
+torch.cuda.synchronize(); t0 = time.perf_counter()
+with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize(); dt = time.perf_counter() - t0
+print("bidir", 2 * 8 * n / dt / 1e9, "GB/s total")
