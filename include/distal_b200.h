@@ -50,6 +50,9 @@ int td_device_count(void);
 int td_set_device(int device);
 /* Number of kernel launches this library issued since load (all threads). */
 long long td_launch_count(void);
+/* Device ordinal a stream belongs to (every compute entry point makes that
+ * device current for the call, so one thread can drive several GPUs). */
+int td_stream_device(void* stream);
 
 /* ---- leaf kernels (replace the per-point interpreter, cin.py:399-417) ---- */
 
@@ -150,6 +153,10 @@ int td_comm_init_rank(void** comm, int nranks, int rank, const char* unique_id, 
 /* single process driving ndev devices */
 int td_comm_init_all(void** comms, int ndev, const int* devices);
 int td_comm_destroy(void* comm);
+/* Sub-communicator over the ranks that pass the same color >= 0 (ranked by
+ * key); color < 0 = not a member (*newcomm = NULL).  Collective over `comm`.
+ * Used for the broadcast groups of fan-out transfers (SUMMA/COSMA panels). */
+int td_comm_split(void* comm, int color, int key, void** newcomm);
 int td_group_start(void);
 int td_group_end(void);
 /* point-to-point transfer of `count` float64 (one CommEvent) */

@@ -30,6 +30,7 @@ _SIGNATURES = {
     "td_device_count": ([], i32),
     "td_set_device": ([i32], i32),
     "td_launch_count": ([], C.c_longlong),
+    "td_stream_device": ([vp], i32),
     "td_dgemm": ([vp, i64, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
     "td_dgemm_config": ([vp, i32, i64, i64, i64, dp, i64, dp, i64, dp, i64, i32], i32),
     "td_dgemm_batched": ([vp, i64, i64, i64, i64, dp, i64, i64, dp, i64, i64, dp, i64, i64, i32], i32),
@@ -49,6 +50,7 @@ _SIGNATURES = {
     "td_comm_init_rank": ([C.POINTER(vp), i32, i32, C.c_char_p, i32], i32),
     "td_comm_init_all": ([C.POINTER(vp), i32, C.POINTER(C.c_int)], i32),
     "td_comm_destroy": ([vp], i32),
+    "td_comm_split": ([vp, i32, i32, C.POINTER(vp)], i32),
     "td_group_start": ([], i32),
     "td_group_end": ([], i32),
     "td_send": ([vp, vp, dp, i64, i32], i32),

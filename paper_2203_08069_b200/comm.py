@@ -34,6 +34,7 @@ class World:
         self.comms = comms or {}        # global GPU index -> ncclComm_t (as int)
         self.torch_devices = torch_devices or {}   # global GPU index -> torch.device
         self._streams = {}
+        self._groups = {}               # sorted GPU tuple -> {owned GPU: sub-communicator}
 
     def owns(self, g: int) -> bool:
         return g in self.torch_devices
@@ -68,7 +69,45 @@ class World:
     def multi_gpu(self) -> bool:
         return self.ngpus > 1
 
+    def group_comm(self, gpus):
+        """{owned GPU: communicator} over the GPU set `gpus` (ranked by GPU
+        index), created on first use with ncclCommSplit.  Collective: every
+        process of the job must request the same sets in the same order --
+        the SPMD executor does, because all ranks walk the same program."""
+        key = tuple(sorted(set(gpus)))
+        if key not in self._groups:
+            color = 0  # every split below is its own call; one color per member set
+            made = {}
+            grouped = len(self.comms) > 1   # one thread splitting several comms must group them
+            if grouped:
+                _native.call("td_group_start")
+            try:
+                for g in sorted(self.comms):
+                    h = C.c_void_p()
+                    member = g in key
+                    _native.call("td_comm_split", C.c_void_p(self.comms[g]), color if member else -1,
+                                 key.index(g) if member else 0, C.byref(h))
+                    made[g] = h
+            finally:
+                if grouped:
+                    _native.call("td_group_end")
+            out = {}
+            for g, h in made.items():
+                if g in key:
+                    if not h.value:
+                        raise ConfigError(f"ncclCommSplit gave no communicator for GPU {g} in {key}")
+                    out[g] = h.value
+            self._groups[key] = out
+        return self._groups[key]
+
     def close(self):
+        for grp in self._groups.values():
+            for h in grp.values():
+                try:
+                    _native.call("td_comm_destroy", C.c_void_p(h))
+                except Exception:
+                    pass
+        self._groups = {}
         for h in self.comms.values():
             try:
                 _native.call("td_comm_destroy", C.c_void_p(h))

@@ -42,9 +42,16 @@ int td_set_device(int device) {
 
 long long td_launch_count(void) { return td::g_launches.load(); }
 
+int td_stream_device(void* stream) {
+  int dev = -1;
+  TD_CUDA(cudaStreamGetDevice(td::as_stream(stream), &dev));
+  return dev;
+}
+
 int td_memcpy_2d(void* stream, double* dst, int64_t dst_pitch, const double* src, int64_t src_pitch,
                  int64_t width, int64_t rows) {
   if (width <= 0 || rows <= 0) return TD_OK;
+  td::StreamDevice sd(stream);
   TD_CUDA(cudaMemcpy2DAsync(dst, size_t(dst_pitch) * 8, src, size_t(src_pitch) * 8, size_t(width) * 8,
                             size_t(rows), cudaMemcpyDefault, td::as_stream(stream)));
   return TD_OK;

@@ -54,6 +54,15 @@ int td_comm_init_all(void** comms, int ndev, const int* devices) {
   return TD_OK;
 }
 
+int td_comm_split(void* comm, int color, int key, void** newcomm) {
+  TD_REQUIRE(comm && newcomm, "comm_split: bad arguments");
+  ncclComm_t out = nullptr;
+  TD_NCCL(ncclCommSplit(static_cast<ncclComm_t>(comm), color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &out,
+                        nullptr));
+  *newcomm = out;
+  return TD_OK;
+}
+
 int td_comm_destroy(void* comm) {
   if (!comm) return TD_OK;
   TD_NCCL(ncclCommDestroy(static_cast<ncclComm_t>(comm)));

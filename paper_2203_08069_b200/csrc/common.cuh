@@ -16,6 +16,28 @@ extern std::atomic<long long> g_launches;
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Makes the stream's device current for the duration of a call (one host
+// thread may drive several GPUs); restores the caller's device afterwards.
+struct StreamDevice {
+  int prev = -1;
+  explicit StreamDevice(void* s) {
+    if (!s) return;
+    int dev = -1, cur = -1;
+    cudaGetDevice(&cur);  // also initialises this (static) runtime before the stream query
+    if (cudaStreamGetDevice(as_stream(s), &dev) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cur != dev) {
+      prev = cur;
+      cudaSetDevice(dev);
+    }
+  }
+  ~StreamDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 inline int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();

@@ -325,12 +325,14 @@ extern "C" {
 
 int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
              const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
+  td::StreamDevice sd(stream);
   td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a);
 }
 
 int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
+  td::StreamDevice sd(stream);
   td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a, config);
 }
@@ -338,6 +340,7 @@ int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K, c
 int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t K, const double* A,
                      int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
                      double* C, int64_t ldc, int64_t strideC, int accumulate) {
+  td::StreamDevice sd(stream);
   td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0};
   int64_t done = 0;
   while (done < batch) {  // grid.y is limited to 65535

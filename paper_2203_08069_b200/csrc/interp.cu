@@ -142,6 +142,7 @@ __global__ void nest_kernel(const __grid_constant__ td_nest_prog p, int64_t npoi
 
 extern "C" int td_nest_eval(void* stream, const void* prog, int64_t bytes) {
   using namespace td;
+  StreamDevice sd(stream);
   TD_REQUIRE(bytes == (int64_t)sizeof(td_nest_prog), "nest_eval: program is %lld bytes, expected %lld",
              (long long)bytes, (long long)sizeof(td_nest_prog));
   const td_nest_prog& p = *static_cast<const td_nest_prog*>(prog);

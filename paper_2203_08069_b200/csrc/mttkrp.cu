@@ -296,6 +296,7 @@ extern "C" int td_mttkrp_config(void* stream, int config, int64_t I, int64_t K, 
                                 const double* D, int64_t ldd, double* A, int64_t lda, int accumulate) {
   using namespace td;
   if (I <= 0 || R <= 0) return TD_OK;
+  StreamDevice sd(stream);
   TD_REQUIRE(I <= 2147483647, "mttkrp: I too large");
   MttkrpArgs a{I, K, L, R, B, sBi, sBk, C, ldc, D, ldd, A, lda, accumulate, nullptr, 0, 0};
   return mttkrp_dispatch(as_stream(stream), a, config);

@@ -251,6 +251,7 @@ int td_ttv(void* stream, int64_t I, int64_t J, int64_t K, const double* B, int64
            const double* c, double* A, int64_t sAi, int64_t sAj, int accumulate) {
   using namespace td;
   if (I <= 0 || J <= 0) return TD_OK;
+  StreamDevice sd(stream);
   const int64_t rows = I * J;
   const bool vec = K % 2 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(c) & 15) == 0 && sBi % 2 == 0 && sBj % 2 == 0;
@@ -266,6 +267,7 @@ int64_t td_innerprod_work_size(void) { return td::IP_MAX_BLOCKS; }
 int td_innerprod(void* stream, int64_t rows, int64_t n, const double* B, int64_t sB, const double* C, int64_t sC,
                  double* out, double* work, int accumulate) {
   using namespace td;
+  StreamDevice sd(stream);
   cudaStream_t st = as_stream(stream);
   const int64_t total = rows > 0 && n > 0 ? rows * n : 0;
   int parts = (int)std::min<int64_t>((int64_t)num_sms() * IP_BLOCKS_PER_SM, IP_MAX_BLOCKS);
@@ -287,6 +289,7 @@ int td_copy_box(void* stream, int ndim, const int64_t* shape, double* dst, const
                 const double* src, const int64_t* src_strides, int accumulate) {
   using namespace td;
   TD_REQUIRE(ndim >= 0 && ndim <= 8, "copy_box: ndim %d out of range", ndim);
+  StreamDevice sd(stream);
   BoxArgs a{};
   int64_t vol = 1;
   if (ndim == 0) {  // scalar
@@ -312,6 +315,7 @@ int td_copy_box(void* stream, int ndim, const int64_t* shape, double* dst, const
 int td_fill(void* stream, double* dst, int64_t n, double value) {
   using namespace td;
   if (n <= 0) return TD_OK;
+  StreamDevice sd(stream);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 16));
   fill_kernel<<<blocks, 256, 0, as_stream(stream)>>>(dst, n, value);
   return check_launch("fill_kernel");
@@ -321,6 +325,7 @@ int td_generate(void* stream, int ndim, const int64_t* gdims, const int64_t* ori
                 double* dst, const int64_t* dst_strides, uint64_t seed, uint64_t tensor_id, int mode) {
   using namespace td;
   TD_REQUIRE(ndim >= 0 && ndim <= 8, "generate: ndim %d out of range", ndim);
+  StreamDevice sd(stream);
   GenArgs a{};
   int64_t total = 1;
   if (ndim == 0) {

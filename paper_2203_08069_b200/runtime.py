@@ -48,6 +48,8 @@ from .tensors import DenseTensor
 from .trace import CommEvent, ExecutionTrace
 
 LEAF_POLICIES = ("auto", "exact")
+# lower one-to-many fetches to ncclBroadcast on GPU sub-communicators (else p2p fan-out)
+USE_BROADCAST = True
 
 
 def _strides(t):
@@ -430,6 +432,7 @@ class _Executor:
         self.W = store.world
         self.policy = policy
         self.m = store.machine
+        self.use_bcast = USE_BROADCAST and self.W.multi_gpu
         self.buffers = {}            # hid -> CUDA tensor (owned GPUs only)
         self.alias_origin = {}       # temp hid aliasing a piece -> (tensor, gpu, color)
         self.out_bufs = {}           # task coord -> CUDA tensor of out_rect
@@ -613,9 +616,45 @@ class _Executor:
         for wave in sorted({t.wave for t in moves}):
             self._transfer_group([t for t in moves if t.wave == wave])
 
-    def _transfer_group(self, moves):
+    def _send_view(self, gs, t):
+        """Contiguous device view of a transfer's part on its source GPU."""
         torch = self.torch
-        sends, recvs = [], []
+        src_h = self.prog.holdings[t.src_hid]
+        self.wait_piece(self.xstream(gs), t.src_hid, t.part)
+        view = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
+        if not view.is_contiguous():
+            st = self.xstream(gs)
+            with torch.cuda.stream(st):
+                packed = torch.empty(t.part.shape, dtype=torch.float64, device=view.device)
+            _copy_box(st, packed, view)
+            view = packed
+        return view
+
+    def _recv_buf(self, gd, part):
+        torch = self.torch
+        st = self.xstream(gd)
+        with torch.cuda.stream(st):
+            buf = torch.empty(part.shape, dtype=torch.float64, device=self.W.device(gd))
+        buf.record_stream(self.cstream(gd))
+        return buf
+
+    def _transfer_group(self, moves):
+        """One NCCL group: same-GPU moves become aliases; a box sent from one
+        holding to >= 2 other GPUs (SUMMA / COSMA panel fan-out, Johnson face
+        broadcast at g > 2) becomes one ncclBroadcast over the sub-communicator
+        of those GPUs; everything else is an ncclSend/ncclRecv pair (Cannon's
+        cyclic shifts, relays, single-destination fetches)."""
+        fan = {}
+        for t in moves:
+            gs, gd = self.gpu(t.src), self.gpu(t.dst)
+            if gs != gd:
+                fan.setdefault((gs, t.src_hid, t.part), []).append(t)
+        bkeys = [k for k, ms in fan.items() if len({self.gpu(m.dst) for m in ms}) >= 2] \
+            if self.use_bcast else []
+        for k in bkeys:     # sub-communicators first: collective over every rank, same order
+            self.W.group_comm({k[0]} | {self.gpu(m.dst) for m in fan[k]})
+        bset = set(bkeys)
+        sends, recvs, bcasts = [], [], []
         for t in moves:
             gs, gd = self.gpu(t.src), self.gpu(t.dst)
             if gs == gd:
@@ -626,28 +665,34 @@ class _Executor:
                     if o is not None:
                         self.alias_origin[t.dst_hid] = o
                 continue
+            if (gs, t.src_hid, t.part) in bset:
+                continue
             if self.W.owns(gs):
-                src_h = self.prog.holdings[t.src_hid]
-                self.wait_piece(self.xstream(gs), t.src_hid, t.part)
-                view = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
-                if not view.is_contiguous():
-                    st = self.xstream(gs)
-                    with torch.cuda.stream(st):
-                        packed = torch.empty(t.part.shape, dtype=torch.float64, device=view.device)
-                    _copy_box(st, packed, view)
-                    view = packed
-                sends.append((gs, gd, view))
+                sends.append((gs, gd, self._send_view(gs, t)))
             if self.W.owns(gd):
-                st = self.xstream(gd)
-                with torch.cuda.stream(st):
-                    buf = torch.empty(t.part.shape, dtype=torch.float64, device=self.W.device(gd))
-                buf.record_stream(self.cstream(gd))
+                buf = self._recv_buf(gd, t.part)
                 self.buffers[t.dst_hid] = buf
                 recvs.append((gd, gs, buf))
-        self._nccl(sends, recvs)
+        for k in bkeys:
+            gs, _, part = k
+            dsts = sorted({self.gpu(m.dst) for m in fan[k]})
+            members = tuple(sorted({gs, *dsts}))
+            comms = self.W.group_comm(members)
+            root = members.index(gs)
+            if self.W.owns(gs):
+                bcasts.append((comms[gs], gs, self._send_view(gs, fan[k][0]), root))
+            for gd in dsts:
+                if not self.W.owns(gd):
+                    continue
+                buf = self._recv_buf(gd, part)
+                for m in fan[k]:
+                    if self.gpu(m.dst) == gd:
+                        self.buffers[m.dst_hid] = buf
+                bcasts.append((comms[gd], gd, buf, root))
+        self._nccl(sends, recvs, bcasts)
 
-    def _nccl(self, sends, recvs):
-        if not sends and not recvs:
+    def _nccl(self, sends, recvs, bcasts=()):
+        if not sends and not recvs and not bcasts:
             return
         _native.call("td_group_start")
         try:
@@ -657,6 +702,9 @@ class _Executor:
             for g, peer, buf in recvs:
                 _native.call("td_recv", self.W.comm(g), stream_handle(self.xstream(g)),
                              C.c_void_p(buf.data_ptr()), max(1, buf.numel()), peer)
+            for comm, g, buf, root in bcasts:
+                _native.call("td_bcast", C.c_void_p(comm), stream_handle(self.xstream(g)),
+                             C.c_void_p(buf.data_ptr()), max(1, buf.numel()), root)
         finally:
             _native.call("td_group_end")
 

@@ -56,7 +56,9 @@ def main():
     for b in (td.summa(2, 1, dims=(192, 160, 256), chunk=32), td.cannon(2, 2, dims=(200, 144, 176)),
               td.johnson(2, 2, 2, dims=(128, 96, 160)), td.mttkrp(2, 2, dims=(40, 32, 48, 36)),
               td.ttm2d(2, 2, dims=(16, 12, 40, 24)), td.innerprod3(4, dims=(24, 10, 70)),
-              td.ttv(4, dims=(20, 12, 90)), td.solomonik(2, 2, 2, dims=(64, 48, 80))):
+              td.ttv(4, dims=(20, 12, 90)), td.solomonik(2, 2, 2, dims=(64, 48, 80)),
+              td.summa(4, 1, dims=(96, 80, 128), chunk=16), td.summa(4, 2, dims=(64, 48, 96), chunk=8),
+              td.cosma_like((4, 1, 1), (1, 1, 2), dims=(64, 40, 72))):
         res, ins = b.run(seed=3)  # same inputs on every rank (SPMD)
         want = seq_eval(td.format_statement(b.statement), b.statement.extents,
                         {n: t.data for n, t in ins.items()})

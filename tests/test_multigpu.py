@@ -1,0 +1,51 @@
+"""Multi-GPU paths (skipped unless >= 2 GPUs are visible).
+
+* single process driving several GPUs (`configure(devices)`, ncclCommInitAll,
+  grouped NCCL calls from one thread, sub-communicator broadcasts);
+* SPMD under torchrun (tests/mp_check.py) at 2 GPUs.
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_single_process_multi_gpu():
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2203_08069_b200 as td
+from oracle.contractions import seq_eval
+n = min(4, __import__('torch').cuda.device_count())
+td.configure(list(range(n)))
+for b in (td.summa(4, 1, dims=(64, 48, 80), chunk=16), td.cannon(2, 2, dims=(40, 36, 44)),
+          td.johnson(2, 2, 2, dims=(24, 20, 28)), td.mttkrp(2, 2, dims=(12, 8, 10, 9)),
+          td.innerprod3(2, dims=(8, 6, 30))):
+    res, ins = b.run(seed=2)
+    want = seq_eval(td.format_statement(b.statement), b.statement.extents, {k: v.data for k, v in ins.items()})
+    assert np.array_equal(res.output.data, np.asarray(want)), b.name
+print("single-process multi-gpu OK")
+""" % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_spmd_torchrun_two_gpus():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "tests", "mp_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "mp_check world=2: OK" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
