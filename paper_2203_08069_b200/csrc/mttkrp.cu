@@ -31,7 +31,7 @@ struct MkCfg {
   static constexpr int THREADS = WARPS * 32;
   static constexpr int A_STAGE = ROWS * MK_SA;
   static constexpr int D_STAGE = MK_BK * MK_SD;
-  static constexpr int SMEM = STAGES * (A_STAGE + D_STAGE) * 8 + WARPS * MK_R * 8;
+  static constexpr int SMEM = STAGES * (A_STAGE + D_STAGE) * 8 + WARPS * MK_R * 8 + ROWS * MK_SD * 8;
 };
 
 struct MttkrpArgs {
@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
   double* Bs = smem;
   double* Ds = smem + STAGES * Cfg::A_STAGE;
   double* red = Ds + STAGES * Cfg::D_STAGE;  // [WARPS][32]
+  double* Cs = red + WARPS * MK_R;            // [ROWS][MK_SD] C block (KPC == 1)
 
   const int64_t i = blockIdx.x / p.groups;
   const int grp = blockIdx.x % p.groups;
@@ -86,6 +87,16 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
     const int64_t l0 = int64_t(t % ltiles) * MK_BK;
     double* bs = Bs + stage * Cfg::A_STAGE;
     double* ds = Ds + stage * Cfg::D_STAGE;
+    if constexpr (KPC == 1) {
+      if (t == 0) {  // the CTA's C block rides in the first stage: the epilogue reads smem, not HBM
+        for (int c = tid; c < ROWS * MK_R; c += Cfg::THREADS) {
+          const int r = c / MK_R, col = c % MK_R;
+          const int64_t gk = k0 + r, gj = j0 + col;
+          const bool ok = gk < K && gj < R;
+          cp_async_f64<1>(Cs + r * MK_SD + col, ok ? p.C + gk * p.ldc + gj : p.C, ok ? 1 : 0);
+        }
+      }
+    }
     if (jfull && k0 + ROWS <= K && l0 + MK_BK <= L) {
       const double* b = Bi + (k0 + fb_r) * p.sBk + fb_c + l0;
 #pragma unroll
@@ -172,12 +183,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
         const int64_t k = k0 + warp * 32 + m * 8 + (lane >> 2);
         const bool kin = k < K;
         const double* crow = p.C + k * p.ldc;
+        const double* srow = Cs + (warp * 32 + m * 8 + (lane >> 2)) * MK_SD;
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int64_t j = j0 + n * 8 + (lane & 3) * 2 + h;
-            if (kin && j < R) part[n][h] += crow[j] * acc[m][n][h];
+            const int jl = n * 8 + (lane & 3) * 2 + h;
+            const int64_t j = j0 + jl;
+            if (kin && j < R) part[n][h] += (KPC == 1 ? srow[jl] : crow[j]) * acc[m][n][h];
             acc[m][n][h] = 0.0;
           }
         }
