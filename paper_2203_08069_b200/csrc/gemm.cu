@@ -15,6 +15,9 @@
 //   * epilogue writes (or accumulates into) row-major C with bounds checks.
 // Summation order: k tiles ascending, within a tile the DMMA's own order --
 // exact on integer-valued data, |err| <= gamma_K |A||B| on real data.
+#include <cmath>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dmma.cuh"
 
@@ -50,6 +53,7 @@ struct GemmArgs {
   int64_t ldc, sC;
   int accumulate;
   int tiles_m, tiles_n;
+  int group;   // M-tiles per raster group (~sqrt of the resident CTAs: square L2 working set per wave)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
@@ -64,7 +68,7 @@ dgemm_kernel(GemmArgs p) {
 
   // grouped rasterisation
   const int tile = blockIdx.x;
-  const int group = 8;
+  const int group = p.group;
   const int per_group = group * p.tiles_n;
   const int g = tile / per_group;
   const int first_m = g * group;
@@ -214,6 +218,23 @@ dgemm_kernel(GemmArgs p) {
   }
 }
 
+// M-tiles per raster group (consecutive CTAs walk down M inside a group, then
+// along N): controls how much A/B one wave keeps live in the 126 MB L2.
+static int raster_group(int blocks_per_sm, int BM, int BN) {
+  static const int forced = [] {
+    const char* e = std::getenv("TD_GEMM_GROUP");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
+  // Measured on B200 at 16384^3 with 64x64 tiles (scratch/group_sweep.sh):
+  // DRAM read per launch 558/290/164/115/128/263 GB for groups 1/2/4/8/16/32
+  // with the same 35.5 TFLOP/s -- 8 M-tiles per group minimises re-reads.
+  (void)blocks_per_sm;
+  (void)BM;
+  (void)BN;
+  return 8;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
 static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
@@ -223,6 +244,7 @@ static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
   TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.tiles_m = (int)ceil_div(a.M, BM);
   a.tiles_n = (int)ceil_div(a.N, BN);
+  a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
   TD_REQUIRE(tiles < (1ll << 31) && batch <= 65535, "dgemm: grid too large (%lld tiles, batch %lld)",
              (long long)tiles, (long long)batch);

@@ -53,7 +53,7 @@ dgemm_ws_kernel(GemmArgs p) {
   uint64_t* empty = full + STAGES;
 
   const int tile = blockIdx.x;
-  const int group = 8;
+  const int group = p.group;
   const int per_group = group * p.tiles_n;
   const int g = tile / per_group;
   const int first_m = g * group;
@@ -193,6 +193,7 @@ static int launch_gemm_ws(cudaStream_t st, int64_t batch, GemmArgs a) {
   TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, W::SMEM_BYTES));
   a.tiles_m = (int)ceil_div(a.M, BM);
   a.tiles_n = (int)ceil_div(a.N, BN);
+  a.group = raster_group(1, BM, BN);
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
   TD_REQUIRE(tiles < (1ll << 31) && batch <= 65535, "dgemm: grid too large (%lld tiles, batch %lld)",
              (long long)tiles, (long long)batch);
