@@ -24,6 +24,11 @@ struct StreamDevice {
     if (!s) return;
     int dev = -1, cur = -1;
     cudaGetDevice(&cur);  // also initialises this (static) runtime before the stream query
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(as_stream(s), &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();  // under CUDA-graph capture: leave the device alone (no stream queries)
+      return;
+    }
     if (cudaStreamGetDevice(as_stream(s), &dev) != cudaSuccess) {
       cudaGetLastError();
       return;
