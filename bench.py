@@ -218,8 +218,6 @@ def bench_gemm(job, steps, warmup, e2e_steps):
     check = _gemm_spot_check(job, store, bundle, n)
 
     # per-launch roofline of the dominant kernel on this rank
-    local_tasks = [t for t in store.machine.enumerate()
-                   if store.machine.device_of(t, job.world.ngpus) in job.world.owned]
     flop_per_launch = _dgemm_flop_per_launch(bundle, n)
     achieved = flop_per_launch / (dgemm_ms / 1e3) / 1e12 if dgemm_ms else None
 
@@ -240,7 +238,7 @@ def bench_gemm(job, steps, warmup, e2e_steps):
                      "peak_source": "measured FP64 DMMA probe (profiles/peaks_r01.json); "
                                     f"cuBLAS DGEMM on the same GPUs: {DGEMM_CUBLAS_TFLOPS} TFLOP/s",
                      "flop_per_launch": flop_per_launch},
-        "clocks": clk.summary(), "e2e": e2e, "local_tasks": len(local_tasks),
+        "clocks": clk.summary(), "e2e": e2e,
     }
 
 

@@ -1,7 +1,6 @@
 """The C-ABI library loads without a GPU and exports every entry point that
 include/distal_b200.h declares (no compute calls here)."""
 
-import ctypes
 import os
 import re
 
@@ -19,7 +18,7 @@ def declared():
 def test_header_declares_the_surface():
     names = declared()
     for want in ("td_dgemm", "td_ttv", "td_ttm", "td_mttkrp", "td_innerprod", "td_nest_eval",
-                 "td_send", "td_recv", "td_bcast", "td_reduce_sum", "td_comm_init_rank"):
+                 "td_send", "td_recv", "td_bcast", "td_reduce_sum", "td_comm_init_rank", "td_comm_split"):
         assert want in names
 
 
@@ -37,18 +36,13 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: a missing library raises DeviceUnavailable."""
     from paper_2203_08069_b200 import _native
     from paper_2203_08069_b200.errors import DeviceUnavailable
-    with pytest.raises(DeviceUnavailable):
-        _native.load.__wrapped__(str(tmp_path / "nope.so")) if hasattr(_native.load, "__wrapped__") \
-            else _load_fresh(str(tmp_path / "nope.so"))
-
-
-def _load_fresh(path):
-    from paper_2203_08069_b200 import _native
     saved = _native._lib
     _native._lib = None
     try:
-        _native.load(path)
+        with pytest.raises(DeviceUnavailable):
+            _native.load(str(tmp_path / "nope.so"))
     finally:
         _native._lib = saved
