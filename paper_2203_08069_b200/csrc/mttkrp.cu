@@ -7,7 +7,8 @@
 //     T[ROWS x 32] = B(i, kblk, :) . D[:, jblk]  on DMMA.8x8x4 tiles (every
 //     warp 32 x 32, 16 DMMA per k4 slice) fed by one cp.async ring over
 //     (k-block, l-tile) pairs, so the pipeline never drains between k-blocks;
-//     epilogue: partial(j) += sum_k C(k,j) * T(k,j) in registers.
+//     epilogue: partial(j) += sum_k C(k,j) * T(k,j) in registers (C read from
+//     a shared-memory copy loaded with the first stage, or from L2).
 // At the end a fixed-order shuffle + shared-memory tree reduces the partial
 // over the warps and the CTA writes it to a stream-ordered workspace
 // [I][groups][R]; `mttkrp_reduce` then sums the groups of every A(i, :) in
@@ -15,23 +16,25 @@
 // order is a fixed function of the shape, runs are bitwise reproducible, and
 // integer-valued inputs give exact results.
 // B is streamed once from HBM (8 B per 64 flop at R = 32); D and C stay in L2.
+// Unlike the GEMM, every B byte comes from DRAM, so the ring must keep many
+// bytes in flight per SM: the configurations trade l-tile depth (BK), stages
+// and resident CTAs per SM (MINB) against shared memory.
 #include "common.cuh"
 #include "dmma.cuh"
 
 namespace td {
 
-constexpr int MK_BK = 16;              // l per pipeline stage
 constexpr int MK_R = 32;               // j columns per CTA
-constexpr int MK_SA = MK_BK + 4;       // B-tile row stride (doubles): conflict-free fragments
-constexpr int MK_SD = MK_R + 4;        // D-tile row stride
+constexpr int MK_SD = MK_R + 4;        // D / C tile row stride (doubles)
 
-template <int WARPS, int STAGES>
+template <int WARPS, int STAGES, int BK, bool CSMEM>
 struct MkCfg {
   static constexpr int ROWS = WARPS * 32;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int A_STAGE = ROWS * MK_SA;
-  static constexpr int D_STAGE = MK_BK * MK_SD;
-  static constexpr int SMEM = STAGES * (A_STAGE + D_STAGE) * 8 + WARPS * MK_R * 8 + ROWS * MK_SD * 8;
+  static constexpr int SA = BK + 4;    // B-tile row stride: conflict-free fragment loads for BK = 8, 16
+  static constexpr int A_STAGE = ROWS * SA;
+  static constexpr int D_STAGE = BK * MK_SD;
+  static constexpr int SMEM = STAGES * (A_STAGE + D_STAGE) * 8 + WARPS * MK_R * 8 + (CSMEM ? ROWS * MK_SD * 8 : 0);
 };
 
 struct MttkrpArgs {
@@ -49,15 +52,17 @@ struct MttkrpArgs {
   int kblocks, groups;
 };
 
-template <int WARPS, int STAGES, int KPC, int VEC>
-__global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(MttkrpArgs p) {
-  using Cfg = MkCfg<WARPS, STAGES>;
+template <int WARPS, int STAGES, int KPC, int BK, bool CSMEM, int MINB, int VEC>
+__global__ void __launch_bounds__(WARPS * 32, MINB) mttkrp_kernel(MttkrpArgs p) {
+  using Cfg = MkCfg<WARPS, STAGES, BK, CSMEM>;
+  static_assert(!CSMEM || KPC == 1, "the shared C block holds one k-block");
   constexpr int ROWS = Cfg::ROWS;
+  constexpr int SA = Cfg::SA;
   extern __shared__ __align__(128) double smem[];
   double* Bs = smem;
   double* Ds = smem + STAGES * Cfg::A_STAGE;
   double* red = Ds + STAGES * Cfg::D_STAGE;  // [WARPS][32]
-  double* Cs = red + WARPS * MK_R;            // [ROWS][MK_SD] C block (KPC == 1)
+  double* Cs = red + WARPS * MK_R;            // [ROWS][MK_SD] C block (CSMEM)
 
   const int64_t i = blockIdx.x / p.groups;
   const int grp = blockIdx.x % p.groups;
@@ -67,15 +72,15 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* __restrict__ Bi = p.B + i * p.sBi;
   const int64_t K = p.K, L = p.L, R = p.R;
-  const int ltiles = (int)ceil_div(L, MK_BK);
+  const int ltiles = (int)ceil_div(L, BK);
   const int total = nkb * ltiles;
 
   // fixed-address fast path (full k-block, full l tile, full 32-wide j block)
-  constexpr int FB_PER_ROW = MK_BK / VEC, FD_PER_ROW = MK_R / VEC;
+  constexpr int FB_PER_ROW = BK / VEC, FD_PER_ROW = MK_R / VEC;
   constexpr int FB_ITERS = ROWS * FB_PER_ROW / Cfg::THREADS, FB_STEP = Cfg::THREADS / FB_PER_ROW;
-  constexpr int FD_ITERS = MK_BK * FD_PER_ROW / Cfg::THREADS, FD_STEP = Cfg::THREADS / FD_PER_ROW;
-  static_assert(FB_ITERS * Cfg::THREADS == ROWS * FB_PER_ROW && FD_ITERS * Cfg::THREADS == MK_BK * FD_PER_ROW,
-                "mttkrp tile / thread mismatch");
+  constexpr int FD_ITERS = BK * FD_PER_ROW / Cfg::THREADS, FD_STEP = Cfg::THREADS / FD_PER_ROW;
+  constexpr bool FD_FAST = FD_ITERS * Cfg::THREADS == BK * FD_PER_ROW && FD_ITERS > 0;
+  static_assert(FB_ITERS * Cfg::THREADS == ROWS * FB_PER_ROW, "mttkrp tile / thread mismatch");
   const int fb_r = tid / FB_PER_ROW, fb_c = (tid % FB_PER_ROW) * VEC;
   const int fd_r = tid / FD_PER_ROW, fd_c = (tid % FD_PER_ROW) * VEC;
   const bool jfull = j0 + MK_R <= R;
@@ -84,11 +89,11 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
 
   auto load = [&](int stage, int t) {
     const int64_t k0 = int64_t(kb0 + t / ltiles) * ROWS;
-    const int64_t l0 = int64_t(t % ltiles) * MK_BK;
+    const int64_t l0 = int64_t(t % ltiles) * BK;
     double* bs = Bs + stage * Cfg::A_STAGE;
     double* ds = Ds + stage * Cfg::D_STAGE;
-    if constexpr (KPC == 1) {
-      if (t == 0) {  // the CTA's C block rides in the first stage: the epilogue reads smem, not HBM
+    if constexpr (CSMEM) {
+      if (t == 0) {  // the CTA's C block rides in the first stage: the epilogue reads smem, not L2
         for (int c = tid; c < ROWS * MK_R; c += Cfg::THREADS) {
           const int r = c / MK_R, col = c % MK_R;
           const int64_t gk = k0 + r, gj = j0 + col;
@@ -97,32 +102,35 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
         }
       }
     }
-    if (jfull && k0 + ROWS <= K && l0 + MK_BK <= L) {
+    if (jfull && k0 + ROWS <= K && l0 + BK <= L) {
       const double* b = Bi + (k0 + fb_r) * p.sBk + fb_c + l0;
 #pragma unroll
       for (int it = 0; it < FB_ITERS; ++it)
-        cp_async_f64<VEC>(bs + (fb_r + it * FB_STEP) * MK_SA + fb_c, b + it * fb_step, VEC);
-      const double* d = fd_base + l0 * p.ldd;
+        cp_async_f64<VEC>(bs + (fb_r + it * FB_STEP) * SA + fb_c, b + it * fb_step, VEC);
+      if constexpr (FD_FAST) {
+        const double* d = fd_base + l0 * p.ldd;
 #pragma unroll
-      for (int it = 0; it < FD_ITERS; ++it)
-        cp_async_f64<VEC>(ds + (fd_r + it * FD_STEP) * MK_SD + fd_c, d + it * fd_step, VEC);
-      return;
-    }
-    constexpr int B_PER_ROW = MK_BK / VEC;
-#pragma unroll 4
-    for (int c = tid; c < ROWS * B_PER_ROW; c += Cfg::THREADS) {
-      const int r = c / B_PER_ROW, col = (c % B_PER_ROW) * VEC;
-      const int64_t gk = k0 + r, gl = l0 + col;
-      int valid = 0;
-      const double* src = p.B;
-      if (gk < K && gl < L) {
-        valid = (int)(L - gl < VEC ? L - gl : VEC);
-        src = Bi + gk * p.sBk + gl;
+        for (int it = 0; it < FD_ITERS; ++it)
+          cp_async_f64<VEC>(ds + (fd_r + it * FD_STEP) * MK_SD + fd_c, d + it * fd_step, VEC);
+        return;
       }
-      cp_async_f64<VEC>(bs + r * MK_SA + col, src, valid);
+    } else {
+      constexpr int B_PER_ROW = BK / VEC;
+#pragma unroll 4
+      for (int c = tid; c < ROWS * B_PER_ROW; c += Cfg::THREADS) {
+        const int r = c / B_PER_ROW, col = (c % B_PER_ROW) * VEC;
+        const int64_t gk = k0 + r, gl = l0 + col;
+        int valid = 0;
+        const double* src = p.B;
+        if (gk < K && gl < L) {
+          valid = (int)(L - gl < VEC ? L - gl : VEC);
+          src = Bi + gk * p.sBk + gl;
+        }
+        cp_async_f64<VEC>(bs + r * SA + col, src, valid);
+      }
     }
     constexpr int D_PER_ROW = MK_R / VEC;
-    for (int c = tid; c < MK_BK * D_PER_ROW; c += Cfg::THREADS) {
+    for (int c = tid; c < BK * D_PER_ROW; c += Cfg::THREADS) {
       const int r = c / D_PER_ROW, col = (c % D_PER_ROW) * VEC;
       const int64_t gl = l0 + r, gj = j0 + col;
       int valid = 0;
@@ -165,10 +173,10 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
     const double* bs = Bs + (t % STAGES) * Cfg::A_STAGE;
     const double* ds = Ds + (t % STAGES) * Cfg::D_STAGE;
 #pragma unroll
-    for (int kk = 0; kk < MK_BK; kk += 4) {
+    for (int kk = 0; kk < BK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) af[m] = bs[(arow + m * 8) * MK_SA + kk + acol];
+      for (int m = 0; m < 4; ++m) af[m] = bs[(arow + m * 8) * SA + kk + acol];
 #pragma unroll
       for (int n = 0; n < 4; ++n) bf[n] = ds[(kk + brow) * MK_SD + bcol + n * 8];
 #pragma unroll
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 4 ? 2 : 1) mttkrp_kernel(
           for (int h = 0; h < 2; ++h) {
             const int jl = n * 8 + (lane & 3) * 2 + h;
             const int64_t j = j0 + jl;
-            if (kin && j < R) part[n][h] += (KPC == 1 ? srow[jl] : crow[j]) * acc[m][n][h];
+            if (kin && j < R) part[n][h] += (CSMEM ? srow[jl] : crow[j]) * acc[m][n][h];
             acc[m][n][h] = 0.0;
           }
         }
@@ -255,9 +263,9 @@ static int retain_pool() {  // keep the stream-ordered pool's memory across sync
   return TD_OK;
 }
 
-template <int WARPS, int STAGES, int KPC>
+template <int WARPS, int STAGES, int KPC, int BK, bool CSMEM, int MINB>
 static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
-  using Cfg = MkCfg<WARPS, STAGES>;
+  using Cfg = MkCfg<WARPS, STAGES, BK, CSMEM>;
   a.kblocks = (int)std::max<int64_t>(1, ceil_div(a.K, Cfg::ROWS));
   a.groups = (int)ceil_div(a.kblocks, KPC);
   TD_REQUIRE(a.I * a.groups < (1ll << 31), "mttkrp: grid too large");
@@ -266,13 +274,13 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
   if (a.K > 0) {
     dim3 grid((unsigned)(a.I * a.groups), (unsigned)ceil_div(a.R, MK_R));
     if (vec2) {
-      TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, KPC, 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-      mttkrp_kernel<WARPS, STAGES, KPC, 2><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+      auto kern = mttkrp_kernel<WARPS, STAGES, KPC, BK, CSMEM, MINB, 2>;
+      TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
     } else {
-      TD_CUDA(cudaFuncSetAttribute(mttkrp_kernel<WARPS, STAGES, KPC, 1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-      mttkrp_kernel<WARPS, STAGES, KPC, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+      auto kern = mttkrp_kernel<WARPS, STAGES, KPC, BK, CSMEM, MINB, 1>;
+      TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
     }
     if (int rc = check_launch("mttkrp_kernel")) return rc;
   } else {
@@ -286,16 +294,20 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
   return rc;
 }
 
+// configurations: <WARPS, STAGES, k-blocks per CTA, l per stage, C in smem, CTAs per SM>
 int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
-  switch (config < 0 ? 1 : config) {
-    case 0: return launch_mttkrp<4, 4, 1>(st, a, vec2);
-    case 1: return launch_mttkrp<4, 3, 1>(st, a, vec2);
-    case 2: return launch_mttkrp<4, 3, 2>(st, a, vec2);
-    case 3: return launch_mttkrp<4, 3, 4>(st, a, vec2);
-    case 4: return launch_mttkrp<4, 4, 2>(st, a, vec2);
-    case 5: return launch_mttkrp<2, 4, 2>(st, a, vec2);
-    case 6: return launch_mttkrp<4, 3, 8>(st, a, vec2);
+  // default 6: 3 stages of 16 l, C from L2, three CTAs per SM (75.5 KiB smem, <= 168
+  // registers each) -> 30.8 TFLOP/s at 1024^3 r32 (scratch/tune2.py sweep of 0..7)
+  switch (config < 0 ? 6 : config) {
+    case 0: return launch_mttkrp<4, 4, 1, 16, false, 2>(st, a, vec2);
+    case 1: return launch_mttkrp<4, 3, 1, 16, true, 2>(st, a, vec2);
+    case 2: return launch_mttkrp<4, 3, 2, 16, false, 2>(st, a, vec2);
+    case 3: return launch_mttkrp<4, 5, 1, 8, false, 3>(st, a, vec2);
+    case 4: return launch_mttkrp<4, 6, 1, 8, false, 3>(st, a, vec2);
+    case 5: return launch_mttkrp<4, 4, 1, 8, true, 3>(st, a, vec2);
+    case 6: return launch_mttkrp<4, 3, 1, 16, false, 3>(st, a, vec2);
+    case 7: return launch_mttkrp<4, 8, 1, 8, false, 2>(st, a, vec2);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;
