@@ -81,6 +81,14 @@ CASES = [
     ("mttkrp", [2, 2], {"dims": [5, 3, 7, 2]}),
     ("mttkrp", [2, 1], {"dims": [6, 5, 4, 3]}),
     ("mttkrp", [1, 1], {"dims": [4, 5, 6, 7]}),
+    # empty trailing blocks / idle processors (ceil-division blocks)
+    ("summa", [4, 1], {"dims": [5, 7, 6], "chunk": 4}),
+    ("cannon", [3, 3], {"dims": [4, 4, 4]}),
+    ("johnson", [2, 2, 2], {"dims": [3, 1, 1]}),
+    ("ttv", [4], {"dims": [3, 2, 5]}),
+    ("innerprod", [4], {"dims": [2, 3]}),
+    ("mttkrp", [3, 2], {"dims": [2, 3, 1, 4]}),
+    ("ttm", [4], {"dims": [3, 1, 2, 2]}),
 ]
 
 SEED = 13
