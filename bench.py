@@ -214,6 +214,18 @@ def bench_gemm(job, steps, warmup, e2e_steps):
     leaves.TIMING = None
     flop = 2.0 * n ** 3
     value = flop * steps / (ms / 1e3) / 1e9
+    # the same steps with communication serialised behind computation: the gap is the
+    # overlap the side-stream NCCL groups buy (zero at p=1, where nothing moves)
+    overlap = None
+    if p > 1:
+        from paper_2203_08069_b200 import runtime as rt
+        rt.OVERLAP_COMM = False
+        try:
+            ms_serial = job.timed(step, steps, 1)
+        finally:
+            rt.OVERLAP_COMM = True
+        overlap = {"ms_per_step_overlapped": ms / steps, "ms_per_step_serialised": ms_serial / steps,
+                   "saved_ms_per_step": (ms_serial - ms) / steps}
     # parity spot check of the last step: exact on integer inputs (Freivalds-style row sample)
     check = _gemm_spot_check(job, store, bundle, n)
 
@@ -238,7 +250,7 @@ def bench_gemm(job, steps, warmup, e2e_steps):
                      "peak_source": "measured FP64 DMMA probe (profiles/peaks_r01.json); "
                                     f"cuBLAS DGEMM on the same GPUs: {DGEMM_CUBLAS_TFLOPS} TFLOP/s",
                      "flop_per_launch": flop_per_launch},
-        "clocks": clk.summary(), "e2e": e2e,
+        "clocks": clk.summary(), "e2e": e2e, "overlap": overlap,
     }
 
 
@@ -522,6 +534,7 @@ def main():
         "per_gpu": gemm["per_gpu"], "check": gemm["check"], "roofline": gemm["roofline"],
         "cpu_baseline": cpu, "e2e": gemm["e2e"], "gpu_launches": gemm["gpu_launches"],
         "gpu_launches_per_step": gemm["launches_per_step"], "clocks": gemm["clocks"],
+        "comm_overlap": gemm["overlap"],
         "kernels": kernels,
     }
     print(json.dumps(line), flush=True)

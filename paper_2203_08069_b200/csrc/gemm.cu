@@ -25,14 +25,19 @@ namespace td {
 
 constexpr int PAD = 4;
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+// KP = 1: "k-pair" fragments -- one LDS.128 fetches A[row][2q], A[row][2q+1]
+// for two consecutive k4 slices (lane q owns k = 2q + s within each k8 group;
+// B is read with the same permutation).  Row strides change so both stay
+// conflict-free: A rows of BK+8 (quarter-warp rows 192 B apart), B rows of
+// BN+2 (k rows 2q land on distinct 8-byte bank groups).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int KP = 0>
 struct GemmCfg {
   static constexpr int GEMM_BK = BK;
   static constexpr int WARPS_M = BM / WM;
   static constexpr int WARPS_N = BN / WN;
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
-  static constexpr int SA = GEMM_BK + PAD;  // A row stride (doubles)
-  static constexpr int SB = BN + PAD;       // B row stride (doubles)
+  static constexpr int SA = GEMM_BK + (KP ? 8 : PAD);  // A row stride (doubles)
+  static constexpr int SB = BN + (KP ? 2 : PAD);       // B row stride (doubles)
   static constexpr int A_STAGE = BM * SA;
   static constexpr int B_STAGE = GEMM_BK * SB;
   static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
@@ -56,11 +61,11 @@ struct GemmArgs {
   int group;   // M-tiles per raster group (~sqrt of the resident CTAs: square L2 working set per wave)
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES>::THREADS,
-                                  GemmCfg<BM, BN, BK, WM, WN, STAGES>::MIN_BLOCKS)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>::THREADS,
+                                  GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>::MIN_BLOCKS)
 dgemm_kernel(GemmArgs p) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>;
   constexpr int GEMM_BK = BK;
   extern __shared__ __align__(128) double smem[];
   double* As = smem;
@@ -182,17 +187,41 @@ dgemm_kernel(GemmArgs p) {
     }
     const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
     const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+    if constexpr (KP) {
 #pragma unroll
-    for (int kk = 0; kk < GEMM_BK; kk += 4) {
-      double af[Cfg::FM], bf[Cfg::FN];
+      for (int kk = 0; kk < GEMM_BK; kk += 8) {
+        double2 a2[Cfg::FM];
+        double b0[Cfg::FN], b1[Cfg::FN];
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(arow + i * 8) * Cfg::SA + kk + acol];
+        for (int i = 0; i < Cfg::FM; ++i)
+          a2[i] = *reinterpret_cast<const double2*>(as + (arow + i * 8) * Cfg::SA + kk + 2 * acol);
 #pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + brow) * Cfg::SB + bcol + j * 8];
+        for (int j = 0; j < Cfg::FN; ++j) {
+          b0[j] = bs[(kk + 2 * brow) * Cfg::SB + bcol + j * 8];
+          b1[j] = bs[(kk + 2 * brow + 1) * Cfg::SB + bcol + j * 8];
+        }
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i)
+        for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a2[i].x, b0[j]);
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a2[i].y, b1[j]);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < GEMM_BK; kk += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(arow + i * 8) * Cfg::SA + kk + acol];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + brow) * Cfg::SB + bcol + j * 8];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
     }
   }
   cp_async_wait<0>();
@@ -235,10 +264,10 @@ static int raster_group(int blocks_per_sm, int BM, int BN) {
   return 8;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0>
 static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC>;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC, KP>;
   static bool configured = false;  // attribute is per-device; cheap to re-set
   (void)configured;
   TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -283,6 +312,13 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(24, 64, 64, 16, 32, 32, 3)              \
   X(25, 64, 64, 32, 32, 32, 2)
 
+// k-pair fragment variants (KP = 1)
+#define TD_GEMM_KP_CONFIGS(X)               \
+  X(30, 64, 64, 16, 32, 32, 4)              \
+  X(31, 64, 128, 16, 32, 64, 3)             \
+  X(32, 128, 64, 16, 64, 32, 3)             \
+  X(33, 64, 64, 16, 32, 32, 3)
+
 // warp-specialised (producer warp + mbarrier ring) variants
 #define TD_GEMM_WS_CONFIGS(X)               \
   X(10, 128, 128, 32, 64, 32, 3)            \
@@ -317,6 +353,11 @@ int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) 
     return vec2 ? launch_gemm<BM, BN, BK, WM, WN, ST, 2>(st, batch, a) : launch_gemm<BM, BN, BK, WM, WN, ST, 1>(st, batch, a);
     TD_GEMM_CONFIGS(TD_GEMM_CASE)
 #undef TD_GEMM_CASE
+#define TD_GEMM_KP_CASE(id, BM, BN, BK, WM, WN, ST) \
+  case id:                                           \
+    return vec2 ? launch_gemm<BM, BN, BK, WM, WN, ST, 2, 1>(st, batch, a) : launch_gemm<BM, BN, BK, WM, WN, ST, 1, 1>(st, batch, a);
+    TD_GEMM_KP_CONFIGS(TD_GEMM_KP_CASE)
+#undef TD_GEMM_KP_CASE
 #define TD_GEMM_WS_CASE(id, BM, BN, BK, WM, WN, ST) \
   case id:                                           \
     return vec2 ? launch_gemm_ws<BM, BN, BK, WM, WN, ST, 2>(st, batch, a) : launch_gemm_ws<BM, BN, BK, WM, WN, ST, 1>(st, batch, a);

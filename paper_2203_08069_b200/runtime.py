@@ -50,6 +50,9 @@ from .trace import CommEvent, ExecutionTrace
 LEAF_POLICIES = ("auto", "exact")
 # lower one-to-many fetches to ncclBroadcast on GPU sub-communicators (else p2p fan-out)
 USE_BROADCAST = True
+# issue step s+1's NCCL group while step s's leaves run (False serialises them: a
+# measurement switch for the overlap, used by bench.py)
+OVERLAP_COMM = True
 
 
 def _strides(t):
@@ -528,6 +531,9 @@ class _Executor:
             self._run_task_major(out_region)
         else:
             for s in range(nsteps):
+                if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
+                    for g in self.owned:
+                        self._sync(self.xstream(g), self.cstream(g))
                 self.transfers(self.prog.transfers[s])
                 for g in self.owned:
                     self._sync(self.cstream(g), self.xstream(g))
