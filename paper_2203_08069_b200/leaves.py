@@ -44,7 +44,7 @@ BUILTIN_LEAVES = frozenset({"auto", "dgemm", "gemm", "ttv", "ttm", "mttkrp", "in
 _ENUM_LIMIT = 1 << 22
 
 # counters for the bench / tests: which path each step took
-STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "nest": 0}
+STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0}
 
 
 # optional per-launch device timing: set TIMING = [] to collect
@@ -184,6 +184,11 @@ def classify(leaf) -> Match | None:
         # innerprod x += Y(v) Z(v)
         if len(out) == 0 and p.var_names == q.var_names:
             return Match("innerprod", {"B": idx[id(p)], "C": idx[id(q)]})
+        # any other pairwise contraction: X(batch, m, n) += P(batch, m, k) Q(batch, k, n)
+        # up to axis order (transposed GEMMs, GEMV, TTM/TTV on any mode, batched products)
+        sp, sq, so = set(p.var_names), set(q.var_names), set(out)
+        if so <= sp | sq and sp <= so | sq and sq <= so | sp and (sp & sq) - so:
+            return Match("contract", {"P": idx[id(p)], "Q": idx[id(q)]})
         return None
     if len(facs) == 3 and len(out) == 2:
         a, b = out
@@ -256,10 +261,134 @@ def _launch_native(m: Match, leaf, box, out: DeviceTile, ins, stream, accumulate
         ok = _innerprod(v["B"], v["C"], o, stream, accumulate)
         if not ok:
             return False
+    elif m.kind == "contract":
+        _contract(leaf.lhs.var_names, accs[m.roles["P"]].var_names, accs[m.roles["Q"]].var_names,
+                  o, v["P"], v["Q"], ext, stream, accumulate)
     else:
         return False
     STATS[m.kind] += 1
     return True
+
+
+# ------------------------------------------------------- generic contraction
+def _group_strides(view, names, groups):
+    """View strides regrouped as one stride per group of axes, if each group is
+    a row-major-contiguous run (else None).  groups: list of var-name lists."""
+    st = dict(zip(names, view.strides()))
+    shape = dict(zip(names, view.rect.shape))
+    out = []
+    for g in groups:
+        if not g:
+            out.append(0)
+            continue
+        stride = st[g[-1]]
+        expect = stride * shape[g[-1]]
+        for v in reversed(g[:-1]):
+            if shape[v] != 1 and st[v] != expect:
+                return None
+            expect = st[v] * shape[v] if shape[v] != 1 else expect
+        out.append(stride)
+    return out
+
+
+def _packed(view, names, order, ext, stream):
+    """Contiguous copy of `view` with its axes permuted into `order`."""
+    torch = torch_mod()
+    shape = [ext[v] for v in order]
+    with torch.cuda.stream(stream):
+        buf = torch.empty(shape, dtype=torch.float64, device=view.data.device)
+    st = dict(zip(names, view.strides()))
+    if shape:
+        _native.call("td_copy_box", stream_handle(stream), len(order), _native.i64_array(shape),
+                     C.c_void_p(buf.data_ptr()), _native.i64_array(buf.stride()), C.c_void_p(view.ptr()),
+                     _native.i64_array([st[v] for v in order]), 0)
+    return buf
+
+
+def _contract_layout(out_names, p_names, q_names, o, pv, qv, ext):
+    """Groups and in-place strides for computing X = P . Q with M from P."""
+    so, sp, sq = set(out_names), set(p_names), set(q_names)
+    batch = [v for v in out_names if v in sp and v in sq]
+    mvars = [v for v in out_names if v in sp and v not in sq]
+    nvars = [v for v in out_names if v in sq and v not in sp]
+    kvars = [v for v in p_names if v in sq and v not in so]
+    gp = _group_strides(pv, p_names, [batch, mvars, kvars])
+    if gp is None or gp[2] != 1 or list(p_names) != batch + mvars + kvars:
+        gp = None
+    gq = _group_strides(qv, q_names, [batch, kvars, nvars])
+    if gq is None or (nvars and gq[2] != 1) or list(q_names) != batch + kvars + nvars:
+        gq = None
+    go = _group_strides(o, out_names, [batch, mvars, nvars])
+    if go is None or (nvars and go[2] != 1) or list(out_names) != batch + mvars + nvars:
+        go = None
+    size = lambda vs: int(np.prod([ext[v] for v in vs])) if vs else 1
+    # elements copied to re-layout operands / the output when not usable in place
+    cost = ((0 if gp else size(p_names)) + (0 if gq else size(q_names)) + (0 if go else 2 * size(out_names)))
+    return cost, (batch, mvars, nvars, kvars, gp, gq, go)
+
+
+def _contract(out_names, p_names, q_names, o, pv, qv, ext, stream, accumulate):
+    """X(b, m, n) (+)= P(b, m, k) Q(b, k, n) for any axis order.  Both operand
+    roles are tried (X = P.Q or, as X's transpose, Q.P) and the one that needs
+    the fewest re-layout copies wins; operands whose axes already form
+    row-major (batch, M, K) / (batch, K, N) matrices are read in place, others
+    are packed by one strided copy; the product is a (batched) DMMA GEMM; an
+    output in another axis order is produced in a scratch matrix and added
+    back with one strided copy."""
+    torch = torch_mod()
+    c1, lay1 = _contract_layout(out_names, p_names, q_names, o, pv, qv, ext)
+    c2, lay2 = _contract_layout(out_names, q_names, p_names, o, qv, pv, ext)
+    if c2 < c1:
+        p_names, q_names, pv, qv, lay = q_names, p_names, qv, pv, lay2
+    else:
+        lay = lay1
+    batch, mvars, nvars, kvars, gp, gq, go = lay
+    size = lambda vs: int(np.prod([ext[v] for v in vs])) if vs else 1
+    Bt, Mt, Nt, Kt = size(batch), size(mvars), size(nvars), size(kvars)
+    keep = []
+    if gp is None:
+        buf = _packed(pv, p_names, batch + mvars + kvars, ext, stream)
+        keep.append(buf)
+        pptr, gp = buf.data_ptr(), [Mt * Kt, Kt, 1]
+    else:
+        pptr = pv.ptr()
+    if gq is None:
+        buf = _packed(qv, q_names, batch + kvars + nvars, ext, stream)
+        keep.append(buf)
+        qptr, gq = buf.data_ptr(), [Kt * Nt, Nt, 1]
+    else:
+        qptr = qv.ptr()
+    direct_out = go is not None
+    if direct_out:
+        optr, ostr, acc = o.ptr(), go, accumulate
+    else:
+        with torch.cuda.stream(stream):
+            scratch = torch.empty((Bt, Mt, Nt), dtype=torch.float64, device=o.data.device)
+        keep.append(scratch)
+        optr, ostr, acc = scratch.data_ptr(), [Mt * Nt, Nt, 1], 0
+    lda = gp[1] if mvars else Kt
+    ldb = gq[1] if kvars else Nt
+    ldc = ostr[1] if mvars else Nt
+    s = stream_handle(stream)
+    if Bt == 1:
+        _native.call("td_dgemm", s, Mt, Nt, Kt, C.c_void_p(pptr), lda, C.c_void_p(qptr), ldb,
+                     C.c_void_p(optr), ldc, acc)
+    else:
+        _native.call("td_dgemm_batched", s, Bt, Mt, Nt, Kt, C.c_void_p(pptr), lda, gp[0], C.c_void_p(qptr),
+                     ldb, gq[0], C.c_void_p(optr), ldc, ostr[0], acc)
+    if not direct_out:
+        st = dict(zip(out_names, o.strides()))
+        order = batch + mvars + nvars
+        src_st = {}
+        run = 1
+        for v in reversed(order):
+            src_st[v] = run
+            run *= ext[v]
+        _native.call("td_copy_box", s, len(out_names), _native.i64_array([ext[v] for v in out_names]),
+                     C.c_void_p(o.ptr()), _native.i64_array([st[v] for v in out_names]),
+                     C.c_void_p(optr), _native.i64_array([src_st[v] for v in out_names]), accumulate)
+    for t in keep:
+        t.record_stream(stream)
 
 
 def _rows_view(t: DeviceTile):
