@@ -14,6 +14,9 @@ leaf statement is matched against the native contractions:
     TTM       X(a,b,d) += Y(a,b,c) * Z(c,d)         -> td_ttm
     MTTKRP    X(a,b) += Y(a,c,d) * Z(c,b) * W(d,b)  -> td_mttkrp (fused)
     innerprod x += Y(v...) * Z(v...)                -> td_innerprod
+    any other X += P * Q with a contracted index     -> (batched) td_dgemm after
+              grouping the indices into batch / M / N / K (transposed GEMMs,
+              GEMV, TTM/TTV on other modes; `_contract`)
 
 Anything else -- or any nest under the ``"interpreter"`` leaf / the
 ``"exact"`` policy -- runs on the exact-order nest kernel (`interp.py`),
