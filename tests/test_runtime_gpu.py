@@ -125,6 +125,20 @@ def test_redistribute_moves_pieces():
     assert trace.memory[(0, 0)] == 8 and trace.memory[(0, 1)] == 4
 
 
+def test_execute_twice_accumulates_like_the_reference():
+    """A second execute on the same store adds into the canonical output
+    (reference commit: canon[rect] += partial, simulator.py:631-632) and the
+    trace accumulates both launches."""
+    for b in (td.summa(2, 2, dims=(24, 20, 28), chunk=8), td.johnson(2, 2, 2, dims=(16, 12, 20))):
+        cin, store = b.prepare(seed=6)
+        trace = td.ExecutionTrace(b.machine)
+        td.execute(cin, store, trace=trace)
+        once = store.gather("C").data.copy()
+        td.execute(cin, store, trace=trace)
+        assert np.array_equal(store.gather("C").data, 2 * once)
+        assert len(trace.launches) == 2 and trace.total_messages % 2 == 0
+
+
 def test_captured_launch_replays():
     """CUDA-graph capture of a whole multi-step, multi-task launch."""
     from paper_2203_08069_b200.runtime import CapturedLaunch
