@@ -50,7 +50,7 @@ def _worker(rank, size, port, queue):
     queue.put((rank, ok))
 
 
-@pytest.mark.parametrize("size", [2, 4])
+@pytest.mark.parametrize("size", [2, 4, 8])
 def test_spmd_send_recv_pairing(size):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
