@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "dmma.cuh"
+#include "gemm.cuh"
 
 namespace td {
 
@@ -48,20 +49,8 @@ struct GemmCfg {
   static constexpr int MIN_BLOCKS = THREADS > 128 ? 1 : (FM * FN <= 16 ? 3 : 2);
 };
 
-struct GemmArgs {
-  int64_t M, N, K;
-  const double* A;
-  int64_t lda, sA;
-  const double* B;
-  int64_t ldb, sB;
-  double* C;
-  int64_t ldc, sC;
-  int accumulate;
-  int tiles_m, tiles_n;
-  int group;   // M-tiles per raster group (~sqrt of the resident CTAs: square L2 working set per wave)
-};
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0, int EPI = 0>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>::THREADS,
                                   GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>::MIN_BLOCKS)
 dgemm_kernel(GemmArgs p) {
@@ -226,6 +215,53 @@ dgemm_kernel(GemmArgs p) {
   }
   cp_async_wait<0>();
 
+  if constexpr (EPI == 1) {
+    // Hadamard with H and sum over the tile's rows: lanes sharing (lane & 3)
+    // hold the same columns (shuffle), then the WARPS_M warps of a column
+    // strip add up in shared memory in warp order -- a fixed summation order.
+    double part[Cfg::FN][2];
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) part[j][0] = part[j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) {
+      const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+      const double* hrow = p.H + r * p.ldh;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (r < M && c + h < N) part[j][h] += hrow[c + h] * acc[i][j][h];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = part[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        part[j][h] = v;
+      }
+    __syncthreads();  // the ring is drained: reuse it as [WARPS_M][BN]
+    double* red = smem;
+    if (lane < 4) {
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) red[(warp / Cfg::WARPS_N) * BN + wn0 + j * 8 + lane * 2 + h] = part[j][h];
+    }
+    __syncthreads();
+    for (int c = tid; c < BN; c += Cfg::THREADS) {
+      double v = red[c];
+#pragma unroll
+      for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
+      if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
+    }
+    return;
+  }
+
   // epilogue
 #pragma unroll
   for (int i = 0; i < Cfg::FM; ++i) {
@@ -264,10 +300,10 @@ static int raster_group(int blocks_per_sm, int BM, int BN) {
   return 8;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC, int KP = 0, int EPI = 0>
 static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, KP>;
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC, KP>;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC, KP, EPI>;
   static bool configured = false;  // attribute is per-device; cheap to re-set
   (void)configured;
   TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -310,7 +346,13 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(22, 128, 64, 32, 64, 32, 2)             \
   X(23, 128, 64, 16, 32, 64, 3)             \
   X(24, 64, 64, 16, 32, 32, 3)              \
-  X(25, 64, 64, 32, 32, 32, 2)
+  X(25, 64, 64, 32, 32, 32, 2)             \
+  X(26, 128, 32, 16, 32, 32, 3)             \
+  X(27, 64, 32, 16, 32, 32, 4)              \
+  X(28, 64, 32, 16, 32, 32, 6)              \
+  X(29, 128, 32, 8, 32, 32, 5)              \
+  X(34, 128, 32, 8, 32, 32, 4)              \
+  X(35, 128, 32, 16, 32, 32, 4)
 
 // k-pair fragment variants (KP = 1)
 #define TD_GEMM_KP_CONFIGS(X)               \
@@ -336,8 +378,11 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // 4 stages) 35.0 TFLOP/s on the TTM shape.
 // 64x64x16 CTA tiles of 4 warps (32x32 each), 4 stages, three CTAs per SM
 // (<= 168 registers): 35.6 TFLOP/s at 16384^3 (96 % of peak; cuBLAS 36.1).
+// N <= 32 (MTTKRP / TTM with a rank-32 factor, GEMV-like panels): 128x32x8
+// tiles, 4 stages, three CTAs per SM -- 33.6 TFLOP/s at 1M x 32 x 1024 where the
+// A panel streams from HBM at 4.2 TB/s (config 21: 31.8; scratch/tune_n32.py).
 static int default_config(int64_t N) {
-  if (N <= 32) return 21;
+  if (N <= 32) return 34;
   return 20;
 }
 
@@ -369,6 +414,55 @@ int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) 
   }
 }
 
+// MTTKRP on the GEMM body (EPI = 1): for every batch b (an i of B(i,k,l)),
+// work[b][tm][n] = sum over the rows r of M-tile tm of H(r,n) * (A_b . B)(r,n).
+// The caller sums the tm partials in ascending order (mttkrp.cu).
+#define TD_ROWSUM_CONFIGS(X)                \
+  X(26, 128, 32, 16, 32, 32, 3)             \
+  X(29, 128, 32, 8, 32, 32, 5)              \
+  X(21, 128, 32, 16, 64, 16, 4)             \
+  X(20, 64, 64, 16, 32, 32, 4)              \
+  X(34, 128, 32, 8, 32, 32, 4)              \
+  X(35, 128, 32, 16, 32, 32, 4)
+
+int dgemm_rowsum_tile_rows(int config) {
+  switch (config) {
+#define TD_ROWSUM_BM(id, BM, BN, BK, WM, WN, ST) \
+  case id:                                        \
+    return BM;
+    TD_ROWSUM_CONFIGS(TD_ROWSUM_BM)
+#undef TD_ROWSUM_BM
+    default:
+      return 0;
+  }
+}
+
+int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
+  const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
+                    (batch == 1 || a.sA % 2 == 0);
+  for (int64_t done = 0; done < batch;) {  // grid.y is limited to 65535
+    const int64_t chunk = std::min<int64_t>(batch - done, 65535);
+    GemmArgs c = a;
+    c.A += done * a.sA;
+    c.C += done * a.sC;
+    int rc = TD_ERR_ARG;
+    switch (config) {
+#define TD_ROWSUM_CASE(id, BM, BN, BK, WM, WN, ST)                                              \
+  case id:                                                                                      \
+    rc = vec2 ? launch_gemm<BM, BN, BK, WM, WN, ST, 2, 0, 1>(st, chunk, c)                      \
+              : launch_gemm<BM, BN, BK, WM, WN, ST, 1, 0, 1>(st, chunk, c);                     \
+    break;
+      TD_ROWSUM_CONFIGS(TD_ROWSUM_CASE)
+#undef TD_ROWSUM_CASE
+      default:
+        set_error("mttkrp: unknown GEMM row-sum config %d", config);
+    }
+    if (rc) return rc;
+    done += chunk;
+  }
+  return TD_OK;
+}
+
 __global__ void zero_rows_kernel(double* C, int64_t M, int64_t N, int64_t ldc, int64_t sC) {
   const int64_t b = blockIdx.y;
   const int64_t total = M * N;
@@ -394,14 +488,14 @@ extern "C" {
 int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
              const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a);
 }
 
 int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0};
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a, config);
 }
 
@@ -409,7 +503,7 @@ int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t 
                      int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
                      double* C, int64_t ldc, int64_t strideC, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0};
+  td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0, 0, nullptr, 0};
   int64_t done = 0;
   while (done < batch) {  // grid.y is limited to 65535
     const int64_t chunk = std::min<int64_t>(batch - done, 65535);

@@ -1,0 +1,31 @@
+// Arguments of the DMMA GEMM body shared by the GEMM / TTM leaves (gemm.cu)
+// and the MTTKRP row-sum variant (mttkrp.cu).
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace td {
+
+struct GemmArgs {
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+  int accumulate;
+  int tiles_m, tiles_n;
+  int group;   // M-tiles per raster group (~sqrt of the resident CTAs: square L2 working set per wave)
+  // EPI = 1 (MTTKRP row-sum epilogue): C[bz][tm][n] = sum over the tile's rows r
+  // of H(r, n) * (A.B)(r, n) -- one partial per M-tile, C is the workspace
+  const double* H;
+  int64_t ldh;
+};
+
+// MTTKRP row-sum GEMMs (EPI = 1 in gemm.cu): rows per M-tile of a config, launch
+int dgemm_rowsum_tile_rows(int config);
+int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a);
+
+}  // namespace td

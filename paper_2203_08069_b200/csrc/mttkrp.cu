@@ -19,8 +19,15 @@
 // Unlike the GEMM, every B byte comes from DRAM, so the ring must keep many
 // bytes in flight per SM: the configurations trade l-tile depth (BK), stages
 // and resident CTAs per SM (MINB) against shared memory.
+//
+// The default (config 12) runs the same algorithm on the tuned GEMM body
+// instead: a batched GEMM over i, M = k rows, N = j, K = l, whose epilogue
+// (gemm.cu, EPI = 1) does the Hadamard with C and the fixed-order sum over the
+// tile's k rows into the same [I][groups][R] workspace; mttkrp_reduce finishes.
+// Measured 33.4 vs 30.9 TFLOP/s for the best fused configuration.
 #include "common.cuh"
 #include "dmma.cuh"
+#include "gemm.cuh"
 
 namespace td {
 
@@ -294,12 +301,45 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
   return rc;
 }
 
-// configurations: <WARPS, STAGES, k-blocks per CTA, l per stage, C in smem, CTAs per SM>
+// MTTKRP as a batched GEMM over i whose epilogue does the Hadamard with C and
+// the sum over the k rows of each tile (gemm.cu, EPI = 1): the tile loop is
+// the tuned GEMM body, so B streams at the GEMM's rate.
+static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
+  const int bm = dgemm_rowsum_tile_rows(gemm_config);
+  TD_REQUIRE(bm > 0, "mttkrp: unknown GEMM row-sum config %d", gemm_config);
+  a.groups = (int)std::max<int64_t>(1, ceil_div(a.K, bm));
+  if (int rc = retain_pool()) return rc;
+  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * a.groups * a.R, st));
+  int rc = TD_OK;
+  if (a.K > 0 && a.L > 0) {
+    GemmArgs g{};
+    g.M = a.K; g.N = a.R; g.K = a.L;
+    g.A = a.B; g.lda = a.sBk; g.sA = a.sBi;
+    g.B = a.D; g.ldb = a.ldd; g.sB = 0;
+    g.C = a.work; g.ldc = a.R; g.sC = int64_t(a.groups) * a.R;
+    g.H = a.C; g.ldh = a.ldc;
+    rc = dgemm_rowsum(st, gemm_config, a.I, g);
+  } else {
+    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.groups * a.R, st));
+  }
+  if (rc == TD_OK) {
+    const int64_t outs = a.I * a.R;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(outs, 256), 148 * 8));
+    mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, a.groups, a.I, a.R, a.A, a.lda, a.accumulate);
+    rc = check_launch("mttkrp_reduce");
+  }
+  TD_CUDA(cudaFreeAsync(a.work, st));
+  return rc;
+}
+
+// configurations 0-7: the fused kernel above, <WARPS, STAGES, k-blocks per CTA,
+// l per stage, C in smem, CTAs per SM>; 8-11: the GEMM body with the row-sum
+// epilogue, GEMM tile configs 26, 29, 21, 20, 34, 35
 int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
-  // default 6: 3 stages of 16 l, C from L2, three CTAs per SM (75.5 KiB smem, <= 168
-  // registers each) -> 30.8 TFLOP/s at 1024^3 r32 (scratch/tune2.py sweep of 0..7)
-  switch (config < 0 ? 6 : config) {
+  // default 12: the GEMM body on 128x32x8 tiles, 4 stages, three CTAs per SM ->
+  // 33.4 TFLOP/s at 1024^3 r32 (fused kernel, best config 6: 30.9; scratch/tune_n32.py)
+  switch (config < 0 ? 12 : config) {
     case 0: return launch_mttkrp<4, 4, 1, 16, false, 2>(st, a, vec2);
     case 1: return launch_mttkrp<4, 3, 1, 16, true, 2>(st, a, vec2);
     case 2: return launch_mttkrp<4, 3, 2, 16, false, 2>(st, a, vec2);
@@ -308,6 +348,12 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
     case 5: return launch_mttkrp<4, 4, 1, 8, true, 3>(st, a, vec2);
     case 6: return launch_mttkrp<4, 3, 1, 16, false, 3>(st, a, vec2);
     case 7: return launch_mttkrp<4, 8, 1, 8, false, 2>(st, a, vec2);
+    case 8: return launch_mttkrp_gemm(st, a, 26);
+    case 9: return launch_mttkrp_gemm(st, a, 29);
+    case 10: return launch_mttkrp_gemm(st, a, 21);
+    case 11: return launch_mttkrp_gemm(st, a, 20);
+    case 12: return launch_mttkrp_gemm(st, a, 34);
+    case 13: return launch_mttkrp_gemm(st, a, 35);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;

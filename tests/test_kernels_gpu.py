@@ -135,6 +135,23 @@ def test_mttkrp_exact(nat, i, k, l, r, accumulate):
     assert np.array_equal(ta.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("config", list(range(14)))
+@pytest.mark.parametrize("i,k,l,r,pad", [(3, 200, 17, 45, 0), (2, 129, 40, 32, 1), (70000, 2, 3, 2, 0)])
+def test_mttkrp_every_config(nat, config, i, k, l, r, pad):
+    """Fused kernels (0-7) and the GEMM-body row-sum variants (8-13): ragged
+    k / l / r tiles, odd strides (scalar cp.async path) and > 65535 batches."""
+    if i > 1000 and config < 8:
+        pytest.skip("the fused kernels have no batch limit to exercise")
+    rng = np.random.default_rng(config + i + k)
+    b, cm, d = ints(rng, i, k, l + pad), ints(rng, k, r), ints(rng, l + pad, r)
+    tb, tcm, td = dev(b), dev(cm), dev(d)
+    ta = torch.full((i, r), 7.0, dtype=torch.float64, device="cuda")
+    nat.call("td_mttkrp_config", stream(), config, i, k, l, r, ptr(tb), k * (l + pad), l + pad, ptr(tcm), r,
+             ptr(td), r, ptr(ta), r, 1)
+    want = 7.0 + ref.mttkrp(b[:, :, :l], cm, d[:l])
+    assert np.array_equal(ta.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("rows,n", [(1, 1), (6, 5), (7, 5), (1, 100003), (33, 4099), (64, 65536)])
 def test_innerprod_exact(nat, rows, n):
     rng = np.random.default_rng(rows + n)
