@@ -20,7 +20,7 @@ import ctypes as C
 import itertools
 
 from . import _native
-from .cin import (Assign, Divide, Forall, LeafKernel, Place, Reduce, Rotate, Seq, Split, Suchthat,
+from .cin import (Assign, Divide, Forall, LeafKernel, Place, Reduce, Seq, Split, Suchthat,
                   INTERPRETER_KERNEL, LeafRuntime, body_of, leaf_statements, lookup_leaf_kernel,
                   relation_defs, relations_of)
 from .distribution import HyperRect, full_rect

@@ -37,7 +37,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .cin import Assign, Divide, Reduce, Rotate, Split
+from .cin import Divide, Reduce, Split
 from .errors import ConfigError, TendistError
 from .interp import DeviceTile, run_nest, stream_handle, torch_mod
 from .ir import Access, Mul, accesses_of

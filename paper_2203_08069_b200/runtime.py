@@ -26,14 +26,13 @@ Drop-in for the reference's runtime (`pkg/src/tendist/simulator.py`):
 from __future__ import annotations
 
 import ctypes as C
-import itertools
 import weakref
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native
-from .cin import (Assign, Forall, INTERPRETER_KERNEL, LeafKernel, Place, Reduce, Suchthat,
+from .cin import (Forall, INTERPRETER_KERNEL, LeafKernel, Suchthat,
                   leaf_accesses, leaf_statements, lookup_leaf_kernel, lower_to_cin)
 from .comm import world as current_world
 from .distribution import HyperRect, TensorDistribution, check_redistributable, subtract_rects
@@ -1040,7 +1039,8 @@ def redistribute(store: RegionStore, name: str, new_dist: TensorDistribution,
         trace.bump_memory(p, store.persistent_volume(p) + fetched[p])
     # data: build the new pieces from old pieces (local copies) and NCCL moves
     W = store.world
-    m = store.machine
+    for g in W.owned:   # pieces may still be landing on the store's compute stream (place_host)
+        torch.cuda.current_stream(W.device(g)).wait_stream(W.streams(g)[0])
     old_region = region
     new_region = Region(store, name, new_dist)
     sends, recvs = [], []
