@@ -13,6 +13,10 @@
 //     registers and issues all of them per k4 slice;
 //   * grouped tile rasterisation (8 M-tiles per group) for L2 reuse;
 //   * epilogue writes (or accumulates into) row-major C with bounds checks.
+// The default path is the TMA-fed variant of the same body (gemm_tma.cuh:
+// k4-sliced tensor-map views, mbarrier-completed stages, 4 CTAs/SM); this
+// LDGSTS kernel serves operands TMA cannot address (odd leading dimensions,
+// K or N not a multiple of 4, unaligned bases).
 // Summation order: k tiles ascending, within a tile the DMMA's own order --
 // exact on integer-valued data, |err| <= gamma_K |A||B| on real data.
 #include <cmath>
@@ -321,6 +325,7 @@ static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace td
+#include "gemm_tma.cuh"
 #include "gemm_ws.cuh"
 namespace td {
 
@@ -370,20 +375,34 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(14, 256, 64, 16, 64, 32, 4)             \
   X(15, 128, 128, 16, 32, 32, 6)
 
-// Measured on B200 (scratch/tune2.py): 128x64x16 tiles, 4 warps of 64x32, 3
-// stages, two CTAs per SM -> 34.2 TFLOP/s at 16384^3 (92% of the 37.1 FP64
-// peak) and 33.1 TFLOP/s for the TTM shape (M = 2^20, N = 64, K = 1024).
-// With the fixed-address load path: 64x128x16 (4 warps of 32x64, = cuBLAS's
-// own d884 tile) 35.2 TFLOP/s at 16384^3 (95 %); 64x64x16 (4 warps of 32x32,
-// 4 stages) 35.0 TFLOP/s on the TTM shape.
-// 64x64x16 CTA tiles of 4 warps (32x32 each), 4 stages, three CTAs per SM
-// (<= 168 registers): 35.6 TFLOP/s at 16384^3 (96 % of peak; cuBLAS 36.1).
-// N <= 32 (MTTKRP / TTM with a rank-32 factor, GEMV-like panels): 128x32x8
-// tiles, 4 stages, three CTAs per SM -- 33.6 TFLOP/s at 1M x 32 x 1024 where the
-// A panel streams from HBM at 4.2 TB/s (config 21: 31.8; scratch/tune_n32.py).
+// TMA-fed variants (gemm_tma.cuh); operands the copy engine cannot address
+// (odd leading dimensions, K or N not a multiple of 4) take the LDGSTS kernel
+#define TD_GEMM_TMA_CONFIGS(X)                 \
+  X(40, 64, 64, 16, 32, 32, 4, 0)              \
+  X(43, 128, 32, 16, 32, 32, 3, 0)             \
+  X(44, 64, 128, 16, 32, 64, 3, 0)             \
+  X(47, 64, 64, 16, 32, 32, 3, 4)              \
+  X(48, 128, 32, 16, 32, 32, 3, 4)             \
+  X(50, 128, 64, 16, 64, 32, 4, 0)
+
+// Tile history on B200 (scratch/tune2.py, tune_n32.py, tune_n64.py; 16384^3
+// unless noted):
+//   LDGSTS 128x64x16, 4 warps of 64x32, 3 stages, 2 CTAs/SM          34.2 TFLOP/s
+//   + fixed-address load path, 64x128x16 (cuBLAS's own d884 tile)       35.2
+//   64x64x16, 4 warps of 32x32, 4 stages, 3 CTAs/SM (config 20)         35.6
+//   TMA 64x64x16, 3 stages, 4 CTAs/SM (<= 128 registers; config 47)     36.5  (98.5 %, cuBLAS 36.1)
+// TTM shape (M = 2^20, N = 64, K = 1024): config 20 35.0, config 47 36.0.
+// N <= 32 (MTTKRP / TTM with a rank-32 factor; the A panel streams from HBM
+// at ~4.4 TB/s): LDGSTS 128x32x8 4 stages (config 34) 33.6, TMA 128x32x16
+// 3 stages (config 48) 35.2.
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;
+}
+
+static int default_tma_config(int64_t N) {
+  if (N <= 32) return 48;
+  return 47;
 }
 
 int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) {
@@ -391,7 +410,7 @@ int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) 
   if (a.K <= 0) return zero_or_keep(st, batch, a.M, a.N, a.C, a.ldc, a.sC, a.accumulate);
   const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                     (batch == 1 || (a.sA % 2 == 0 && a.sB % 2 == 0));
-  if (config < 0) config = default_config(a.N);
+  if (config < 0) config = tma_ok(batch, a) ? default_tma_config(a.N) : default_config(a.N);
   switch (config) {
 #define TD_GEMM_CASE(id, BM, BN, BK, WM, WN, ST) \
   case id:                                        \
@@ -403,6 +422,13 @@ int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) 
     return vec2 ? launch_gemm<BM, BN, BK, WM, WN, ST, 2, 1>(st, batch, a) : launch_gemm<BM, BN, BK, WM, WN, ST, 1, 1>(st, batch, a);
     TD_GEMM_KP_CONFIGS(TD_GEMM_KP_CASE)
 #undef TD_GEMM_KP_CASE
+#define TD_GEMM_TMA_CASE(id, BM, BN, BK, WM, WN, ST, MINB)                                     \
+  case id:                                                                                      \
+    if (tma_ok(batch, a)) return launch_gemm_tma<BM, BN, BK, WM, WN, ST, 0, MINB>(st, batch, a); \
+    return vec2 ? launch_gemm<BM, BN, BK, WM, WN, 3, 2>(st, batch, a)                           \
+                : launch_gemm<BM, BN, BK, WM, WN, 3, 1>(st, batch, a);
+    TD_GEMM_TMA_CONFIGS(TD_GEMM_TMA_CASE)
+#undef TD_GEMM_TMA_CASE
 #define TD_GEMM_WS_CASE(id, BM, BN, BK, WM, WN, ST) \
   case id:                                           \
     return vec2 ? launch_gemm_ws<BM, BN, BK, WM, WN, ST, 2>(st, batch, a) : launch_gemm_ws<BM, BN, BK, WM, WN, ST, 1>(st, batch, a);
@@ -431,6 +457,9 @@ int dgemm_rowsum_tile_rows(int config) {
   case id:                                        \
     return BM;
     TD_ROWSUM_CONFIGS(TD_ROWSUM_BM)
+#define TD_ROWSUM_TMA_BM(id, BM, BN, BK, WM, WN, ST, MINB) TD_ROWSUM_BM(id, BM, BN, BK, WM, WN, ST)
+    TD_GEMM_TMA_CONFIGS(TD_ROWSUM_TMA_BM)
+#undef TD_ROWSUM_TMA_BM
 #undef TD_ROWSUM_BM
     default:
       return 0;
@@ -454,6 +483,14 @@ int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
     break;
       TD_ROWSUM_CONFIGS(TD_ROWSUM_CASE)
 #undef TD_ROWSUM_CASE
+#define TD_ROWSUM_TMA_CASE(id, BM, BN, BK, WM, WN, ST, MINB)                                    \
+  case id:                                                                                      \
+    rc = tma_ok(chunk, c) ? launch_gemm_tma<BM, BN, BK, WM, WN, ST, 1, MINB>(st, chunk, c)      \
+                          : (vec2 ? launch_gemm<BM, BN, BK, WM, WN, 3, 2, 0, 1>(st, chunk, c)   \
+                                  : launch_gemm<BM, BN, BK, WM, WN, 3, 1, 0, 1>(st, chunk, c)); \
+    break;
+      TD_GEMM_TMA_CONFIGS(TD_ROWSUM_TMA_CASE)
+#undef TD_ROWSUM_TMA_CASE
       default:
         set_error("mttkrp: unknown GEMM row-sum config %d", config);
     }

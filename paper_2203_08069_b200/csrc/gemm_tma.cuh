@@ -1,0 +1,267 @@
+// TMA-fed variant of the DMMA GEMM body (included by gemm.cu).
+//
+// Operand tiles arrive by `cp.async.bulk.tensor` (one elected thread issues
+// two bulk copies per stage, completion counted on an mbarrier with
+// expect_tx) instead of per-thread LDGSTS.  The tensor maps are k4-sliced
+// views of the row-major operands, so the copies land in the layouts the
+// DMMA fragments want:
+//   A tile  [BK/4][BM][4]   (view dims {4 k, M, K/4, batch}, strides {lda, 4, sA})
+//   B tile  [BN/4][BK][4]   (view dims {4 n, K, N/4, batch}, strides {ldb, 4, sB})
+// A fragment (8 rows x 4 k) and B fragment (4 k x 8 cols) of a warp are then
+// two contiguous 128-byte runs: conflict-free LDS.64 with no padding, and the
+// out-of-bounds parts of edge tiles are zero-filled by the copy engine (no
+// predicated loads).  Needs 16-byte aligned bases, even leading dimensions
+// and K, N multiples of 4; gemm.cu falls back to the LDGSTS kernel otherwise.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace td {
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_4d(void* sdst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(sdst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
+struct TmaCfg {
+  static constexpr int WARPS_M = BM / WM;
+  static constexpr int WARPS_N = BN / WN;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int FM = WM / 8;
+  static constexpr int FN = WN / 8;
+  static constexpr int A_STAGE = BM * BK;  // doubles
+  static constexpr int B_STAGE = BK * BN;
+  static constexpr int STAGE_BYTES = (A_STAGE + B_STAGE) * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 128;  // + alignment slack
+  static constexpr int MIN_BLOCKS = MINB ? MINB : (THREADS > 128 ? 1 : (FM * FN <= 16 ? 3 : 2));
+  static_assert(BK % 4 == 0 && BN % 8 == 0 && BM <= 256 && BK * BN / 4 <= 256 * 64, "tma tile");
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB = 0>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
+                                  TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
+dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
+  extern __shared__ __align__(128) unsigned char tma_smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 127) & ~uintptr_t(127));
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_STAGE;
+
+  // grouped rasterisation (as dgemm_kernel)
+  const int tile = blockIdx.x;
+  const int per_group = p.group * p.tiles_n;
+  const int first_m = (tile / per_group) * p.group;
+  const int gsize = min(p.tiles_m - first_m, p.group);
+  const int in_g = tile % per_group;
+  const int tm = first_m + in_g % gsize;
+  const int tn = in_g / gsize;
+  const int m0 = tm * BM;
+  const int n0 = tn * BN;
+  const int bz = blockIdx.y;
+  const int bzB = p.sB ? bz : 0;
+  double* __restrict__ C = p.C + int64_t(bz) * p.sC;
+  const int64_t M = p.M, N = p.N, K = p.K;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp / Cfg::WARPS_N) * WM;
+  const int wn0 = (warp % Cfg::WARPS_N) * WN;
+  const int ktiles = (int)ceil_div(K, BK);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
+    mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    tma_load_4d(As + s * Cfg::A_STAGE, &tmA, 0, m0, kt * (BK / 4), bz, &full[s]);
+    tma_load_4d(Bs + s * Cfg::B_STAGE, &tmB, 0, kt * BK, n0 / 4, bzB, &full[s]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s)
+      if (s < ktiles) issue(s);
+  }
+
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // fragment offsets inside a stage (doubles)
+  const int a_off = (wm0 + (lane >> 2)) * 4 + (lane & 3);                 // + kq*BM*4 + i*32
+  const int b_off = ((wn0 + (lane >> 2)) / 4) * BK * 4 + (lane & 3) * 4 + ((lane >> 2) & 3);  // + kq*16 + j*2*BK*4
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    mbar_wait(&full[kt % STAGES], (kt / STAGES) & 1);
+    __syncthreads();  // every warp is done with the stage the next copy overwrites
+    if (tid == 0 && kt + STAGES - 1 < ktiles) issue(kt + STAGES - 1);
+    const double* as = As + (kt % STAGES) * Cfg::A_STAGE + a_off;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE + b_off;
+#pragma unroll
+    for (int kq = 0; kq < BK / 4; ++kq) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = as[kq * BM * 4 + i * 32];
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[kq * 16 + j * 2 * BK * 4];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+
+  if constexpr (EPI == 1) {  // MTTKRP row-sum epilogue (see dgemm_kernel)
+    double part[Cfg::FN][2];
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) part[j][0] = part[j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) {
+      const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+      const double* hrow = p.H + r * p.ldh;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (r < M && c + h < N) part[j][h] += hrow[c + h] * acc[i][j][h];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = part[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        part[j][h] = v;
+      }
+    __syncthreads();  // every stage has been consumed: reuse the ring as [WARPS_M][BN]
+    double* red = smem;
+    if (lane < 4) {
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) red[(warp / Cfg::WARPS_N) * BN + wn0 + j * 8 + lane * 2 + h] = part[j][h];
+    }
+    __syncthreads();
+    for (int c = tid; c < BN; c += Cfg::THREADS) {
+      double v = red[c];
+#pragma unroll
+      for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
+      if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
+    }
+    return;
+  }
+
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+    if (r >= M) continue;
+    double* crow = C + r * p.ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h < N) {
+          double v = acc[i][j][h];
+          if (p.accumulate) v += crow[c + h];
+          crow[c + h] = v;
+        }
+      }
+    }
+  }
+}
+
+// ---- host side: tensor maps through the driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// k4-sliced 4-D view {4, rows, cols/4, batch} of a row-major [batch][rows][cols] operand
+static int make_sliced_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                           int64_t batch, int64_t batch_stride, int box_rows, int box_cols) {
+  auto enc = tma_encoder();
+  TD_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[4] = {4, (cuuint64_t)rows, (cuuint64_t)(cols / 4), (cuuint64_t)batch};
+  const cuuint64_t strides[3] = {(cuuint64_t)ld * 8, 32, (cuuint64_t)(batch > 1 ? batch_stride * 8 : 16)};
+  const cuuint32_t box[4] = {4, (cuuint32_t)box_rows, (cuuint32_t)(box_cols / 4), 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TD_OK;
+}
+
+static bool tma_ok(int64_t batch, const GemmArgs& a) {
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return al(a.A) && al(a.B) && a.lda % 2 == 0 && a.ldb % 2 == 0 && a.K % 4 == 0 && a.N % 4 == 0 &&
+         a.M < (1ll << 31) && a.K < (1ll << 31) && a.N < (1ll << 31) &&
+         (batch == 1 || (a.sA % 2 == 0 && a.sB % 2 == 0)) && tma_encoder() != nullptr;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB = 0>
+static int launch_gemm_tma(cudaStream_t st, int64_t batch, GemmArgs a) {
+  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
+  auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, EPI, MINB>;
+  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  CUtensorMap ma, mb;
+  if (int rc = make_sliced_map(&ma, a.A, a.M, a.K, a.lda, batch, a.sA, BM, BK)) return rc;
+  if (int rc = make_sliced_map(&mb, a.B, a.K, a.N, a.ldb, a.sB ? batch : 1, a.sB, BK, BN)) return rc;
+  a.tiles_m = (int)ceil_div(a.M, BM);
+  a.tiles_n = (int)ceil_div(a.N, BN);
+  a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
+  TD_REQUIRE(tiles < (1ll << 31) && batch <= 65535, "dgemm: grid too large (%lld tiles, batch %lld)",
+             (long long)tiles, (long long)batch);
+  dim3 grid((unsigned)tiles, (unsigned)batch);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ma, mb, a);
+  return check_launch("dgemm_tma_kernel");
+}
+
+}  // namespace td

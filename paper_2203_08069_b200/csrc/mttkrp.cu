@@ -20,11 +20,12 @@
 // bytes in flight per SM: the configurations trade l-tile depth (BK), stages
 // and resident CTAs per SM (MINB) against shared memory.
 //
-// The default (config 12) runs the same algorithm on the tuned GEMM body
+// The default (config 18) runs the same algorithm on the tuned GEMM body
 // instead: a batched GEMM over i, M = k rows, N = j, K = l, whose epilogue
-// (gemm.cu, EPI = 1) does the Hadamard with C and the fixed-order sum over the
-// tile's k rows into the same [I][groups][R] workspace; mttkrp_reduce finishes.
-// Measured 33.4 vs 30.9 TFLOP/s for the best fused configuration.
+// (gemm.cu / gemm_tma.cuh, EPI = 1) does the Hadamard with C and the
+// fixed-order sum over the tile's k rows into the same [I][groups][R]
+// workspace; mttkrp_reduce finishes.  Measured 34.8 (TMA-fed body) and 33.4
+// (LDGSTS body) vs 30.9 TFLOP/s for the best fused configuration.
 #include "common.cuh"
 #include "dmma.cuh"
 #include "gemm.cuh"
@@ -333,13 +334,16 @@ static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
 }
 
 // configurations 0-7: the fused kernel above, <WARPS, STAGES, k-blocks per CTA,
-// l per stage, C in smem, CTAs per SM>; 8-11: the GEMM body with the row-sum
-// epilogue, GEMM tile configs 26, 29, 21, 20, 34, 35
+// l per stage, C in smem, CTAs per SM>; 8-13, 15, 18: the GEMM body with the
+// row-sum epilogue on GEMM tile configs 26, 29, 21, 20, 34, 35, 43, 48 (the
+// last two TMA-fed)
 int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
-  // default 12: the GEMM body on 128x32x8 tiles, 4 stages, three CTAs per SM ->
-  // 33.4 TFLOP/s at 1024^3 r32 (fused kernel, best config 6: 30.9; scratch/tune_n32.py)
-  switch (config < 0 ? 12 : config) {
+  // default 18: the TMA-fed GEMM body on 128x32x16 tiles, 3 stages, <= 128
+  // registers -> 34.8 TFLOP/s at 1024^3 r32 (LDGSTS body, config 12: 33.4; fused
+  // kernel, best config 6: 30.9; scratch/tune_n32.py).  Operands the copy
+  // engine cannot address take the LDGSTS body with the same tile.
+  switch (config < 0 ? 18 : config) {
     case 0: return launch_mttkrp<4, 4, 1, 16, false, 2>(st, a, vec2);
     case 1: return launch_mttkrp<4, 3, 1, 16, true, 2>(st, a, vec2);
     case 2: return launch_mttkrp<4, 3, 2, 16, false, 2>(st, a, vec2);
@@ -354,6 +358,8 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
     case 11: return launch_mttkrp_gemm(st, a, 20);
     case 12: return launch_mttkrp_gemm(st, a, 34);
     case 13: return launch_mttkrp_gemm(st, a, 35);
+    case 15: return launch_mttkrp_gemm(st, a, 43);
+    case 18: return launch_mttkrp_gemm(st, a, 48);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;

@@ -79,6 +79,25 @@ def test_dgemm_strided_views_scalar_path(nat, m, n, k):
     assert not got[m:, :].any() and not got[:, :1].any()
 
 
+@pytest.mark.parametrize("config", [20, 34, 40, 43, 44, 47, 48, 50])
+@pytest.mark.parametrize("m,n,k,off", [(100, 36, 44, 0), (257, 68, 1000, 0), (64, 64, 16, 0), (3, 4, 4, 0),
+                                       (130, 72, 52, 2), (65, 100, 30, 0)])
+def test_dgemm_every_tile_config(nat, config, m, n, k, off):
+    """LDGSTS and TMA tile configurations on ragged edges (M, N, K not
+    multiples of the tile), offset views (16-byte aligned, even leading
+    dimensions) and shapes the copy engine cannot address (K % 4 != 0 falls
+    back to the LDGSTS kernel)."""
+    rng = np.random.default_rng(config + m + n + k)
+    big_a, big_b = ints(rng, m + off, k + 2 * off), ints(rng, k + off, n + 2 * off)
+    c0 = ints(rng, m, n)
+    ta, tb, tc = dev(big_a), dev(big_b), dev(c0)
+    pa = C.c_void_p(ta.data_ptr() + 8 * (off * (k + 2 * off) + off))
+    pb = C.c_void_p(tb.data_ptr() + 8 * (off * (n + 2 * off) + off))
+    nat.call("td_dgemm_config", stream(), config, m, n, k, pa, k + 2 * off, pb, n + 2 * off, ptr(tc), n, 1)
+    want = c0 + ref.gemm(big_a[off:off + m, off:off + k], big_b[off:off + k, off:off + n])
+    assert np.array_equal(tc.cpu().numpy(), want)
+
+
 def test_dgemm_real_tolerance(nat):
     rng = np.random.default_rng(3)
     m, n, k = 300, 260, 1500
@@ -135,11 +154,13 @@ def test_mttkrp_exact(nat, i, k, l, r, accumulate):
     assert np.array_equal(ta.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("config", list(range(14)))
-@pytest.mark.parametrize("i,k,l,r,pad", [(3, 200, 17, 45, 0), (2, 129, 40, 32, 1), (70000, 2, 3, 2, 0)])
+@pytest.mark.parametrize("config", list(range(14)) + [15, 18])
+@pytest.mark.parametrize("i,k,l,r,pad", [(3, 200, 17, 45, 0), (2, 129, 40, 32, 1), (70000, 2, 3, 2, 0),
+                                         (3, 130, 44, 36, 0), (70000, 3, 4, 4, 0)])
 def test_mttkrp_every_config(nat, config, i, k, l, r, pad):
-    """Fused kernels (0-7) and the GEMM-body row-sum variants (8-13): ragged
-    k / l / r tiles, odd strides (scalar cp.async path) and > 65535 batches."""
+    """Fused kernels (0-7) and the GEMM-body row-sum variants (8-13, 15, 18; 15
+    and 18 fed by TMA): ragged k / l / r tiles, odd strides (scalar cp.async path), shapes
+    the copy engine can address (l, r multiples of 4) and > 65535 batches."""
     if i > 1000 and config < 8:
         pytest.skip("the fused kernels have no batch limit to exercise")
     rng = np.random.default_rng(config + i + k)
