@@ -167,6 +167,28 @@ int td_bcast(void* comm, void* stream, double* buf, int64_t count, int root);
 int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count, int root);
 int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count);
 
+/* ---- peer memory over NVLink (csrc/peer.cu) ------------------------------
+ * Reduce write-backs of the commit phase (reference simulator.py:624-654,
+ * reduce events :635-645) whose whole partial goes to another GPU's home
+ * piece: the task's leaf epilogue stores its tiles straight into an inbox in
+ * the home GPU's HBM while the rest of the GEMM still computes; an 8-byte
+ * NCCL token then orders the home's task-order accumulation after it.
+ * One process, several GPUs: td_peer_enable + td_peer_alloc(handle = NULL).
+ * One process per GPU: the home calls td_peer_alloc with a handle buffer and
+ * the writer maps it with td_peer_open. */
+#define TD_IPC_HANDLE_BYTES 64
+/* 1 if `device` can map `peer`'s memory, 0 if not, < 0 on error. */
+int td_peer_can_access(int device, int peer);
+/* Let kernels on `device` access `peer`'s allocations (idempotent). */
+int td_peer_enable(int device, int peer);
+/* cudaMalloc `bytes` on `device`; if ipc_handle != NULL also export a CUDA
+ * IPC handle (TD_IPC_HANDLE_BYTES bytes) for td_peer_open in another process. */
+int td_peer_alloc(int device, int64_t bytes, void** ptr, char* ipc_handle);
+int td_peer_free(int device, void* ptr);
+/* Map another process's td_peer_alloc buffer into `device`'s context. */
+int td_peer_open(int device, const char* ipc_handle, void** ptr);
+int td_peer_close(int device, void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,12 @@ _SIGNATURES = {
     "td_bcast": ([vp, vp, dp, i64, i32], i32),
     "td_reduce_sum": ([vp, vp, dp, dp, i64, i32], i32),
     "td_allreduce_sum": ([vp, vp, dp, dp, i64], i32),
+    "td_peer_can_access": ([i32, i32], i32),
+    "td_peer_enable": ([i32, i32], i32),
+    "td_peer_alloc": ([i32, i64, C.POINTER(vp), C.c_char_p], i32),
+    "td_peer_free": ([i32, vp], i32),
+    "td_peer_open": ([i32, C.c_char_p, C.POINTER(vp)], i32),
+    "td_peer_close": ([i32, vp], i32),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -35,6 +35,7 @@ class World:
         self.torch_devices = torch_devices or {}   # global GPU index -> torch.device
         self._streams = {}
         self._groups = {}               # sorted GPU tuple -> {owned GPU: sub-communicator}
+        self.inbox_sets = {}            # id(program) -> peer.InboxSet (peer-memory write-backs)
 
     def owns(self, g: int) -> bool:
         return g in self.torch_devices
@@ -69,6 +70,15 @@ class World:
     def multi_gpu(self) -> bool:
         return self.ngpus > 1
 
+    def all_gather_object(self, obj) -> list:
+        """obj of every process, in rank order (torch.distributed; [obj] alone)."""
+        if self.nprocs == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.nprocs
+        dist.all_gather_object(out, obj)
+        return out
+
     def group_comm(self, gpus):
         """{owned GPU: communicator} over the GPU set `gpus` (ranked by GPU
         index), created on first use with ncclCommSplit.  Collective: every
@@ -101,6 +111,9 @@ class World:
         return self._groups[key]
 
     def close(self):
+        for s in self.inbox_sets.values():
+            s.free()
+        self.inbox_sets = {}
         for grp in self._groups.values():
             for h in grp.values():
                 try:

@@ -476,26 +476,47 @@ def _box_cached(loops, leaf, defs):
     return box
 
 
-def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream) -> str:
+def _zero_tile(out: DeviceTile, stream) -> None:
+    """out = +0.0 on `stream` (contiguous tiles, including peer inboxes)."""
+    data = out.data
+    if not data.is_contiguous():
+        raise TendistError(f"cannot zero the strided output tile {out!r}")
+    _native.call("td_fill", stream_handle(stream), C.c_void_p(data.data_ptr()), data.numel(), 0.0)
+
+
+def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream, accumulate: int = 1) -> str:
     """Execute one step nest; returns the path taken ("dgemm", ..., "nest").
 
-    policy: "auto" | a builtin contraction name | "interpreter" / "exact"."""
+    policy: "auto" | a builtin contraction name | "interpreter" / "exact".
+    accumulate=0: `out` holds garbage and this nest is its only writer (a
+    peer-memory inbox, `peer.py`): a native leaf covering the whole tile
+    overwrites it (0 + x = x, so the bits equal accumulating into zeros);
+    anything else zeroes it first."""
+    zeroed = bool(accumulate)
     if isinstance(leaf, Reduce) and policy not in ("interpreter", "exact"):
         m = _classify_cached(leaf)
         want = {"gemm": "dgemm"}.get(policy, policy)
         if m is not None and (want == "auto" or want == m.kind):
             box = _box_cached(loops, leaf, defs)
             if box == {}:
+                if not zeroed:
+                    _zero_tile(out, stream)
                 return "empty"
             if box is not None:
+                acc = accumulate
+                if not zeroed and _sub(out, leaf.lhs, box).rect != out.rect:
+                    _zero_tile(out, stream)
+                    zeroed, acc = True, 1
                 ev = _timing_start(stream)
-                if _launch_native(m, leaf, box, out, ins, stream):
+                if _launch_native(m, leaf, box, out, ins, stream, acc):
                     _timing_stop(m.kind, ev, stream)
                     return m.kind
         if want not in ("auto",):
             raise ConfigError(f"leaf kernel {policy!r} does not apply to {leaf!r} on this nest")
     elif policy not in ("auto", "interpreter", "exact"):
         raise ConfigError(f"leaf kernel {policy!r} needs a reduction statement")
+    if not zeroed:
+        _zero_tile(out, stream)
     run_nest(loops, leaf, defs, out, ins, stream)
     STATS["nest"] += 1
     return "nest"

@@ -31,7 +31,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native
+from . import _native, peer
 from .cin import (Forall, INTERPRETER_KERNEL, LeafKernel, Suchthat,
                   leaf_accesses, leaf_statements, lookup_leaf_kernel, lower_to_cin)
 from .comm import world as current_world
@@ -515,12 +515,19 @@ class _Executor:
             self._sync(self.xstream(g), cur)
         out_region = self.store[self.plan.out_name]
         self.direct = self._direct_commits(out_region)
+        self.inbox = self._inboxes()
         for t in self.plan.tasks:
             g = self.gpu(t.coord)
             if t.out_rect is not None and self.W.owns(g):
                 if t.coord in self.direct:
                     color = self.direct[t.coord]
                     self.out_bufs[t.coord] = out_region.piece(g, color)
+                    continue
+                ib = self.inbox.get(t.coord)
+                if ib is not None:
+                    if ib.credit is not None:       # the home has released the inbox
+                        self.cstream(g).wait_event(ib.credit)
+                    self.out_bufs[t.coord] = ib.writer_view()
                     continue
                 with torch.cuda.stream(self.cstream(g)):
                     self.out_bufs[t.coord] = torch.zeros(t.out_rect.shape, dtype=torch.float64,
@@ -549,6 +556,17 @@ class _Executor:
             self._sync(cur, self.xstream(g))
         self.buffers.clear()
         self.out_bufs.clear()
+
+    def _inboxes(self) -> dict:
+        """{task coord: peer.Inbox} of the write-backs that go through peer
+        memory (leaf epilogue stores into the home GPU, `peer.py`)."""
+        if not (peer.PEER_REDUCE and self.W.multi_gpu) or not self.prog.commits:
+            return {}
+        task_loops, _ = _loops_of(self.plan.task_body)
+        _, plugins = _leaf_choice(self.plan.relations, [v for v, _, _ in task_loops], self.policy)
+        if plugins:             # user leaf kernels are handed PyTorch tensors
+            return {}
+        return peer.inbox_set(self.prog, self.W, self.gpu).by_task()
 
     def _local_only(self) -> bool:
         """No transfer or commit crosses GPUs (e.g. every single-GPU run)."""
@@ -771,9 +789,13 @@ class _Executor:
             g = self.gpu(w.task.coord)
             if not self.W.owns(g) or w.task.out_rect is None:
                 continue
-            if any(rect is None for _, rect, _ in w.operands.values()):
-                continue      # some access is empty on this step: no iteration points
             st = self.cstream(g)
+            acc = 0 if w.task.coord in self.inbox else 1     # an inbox is overwritten, not zeroed
+            if any(rect is None for _, rect, _ in w.operands.values()):
+                if not acc:   # some access is empty on this step: the partial is all zeros
+                    _native.call("td_fill", stream_handle(st), C.c_void_p(self.out_bufs[w.task.coord].data_ptr()),
+                                 self.out_bufs[w.task.coord].numel(), 0.0)
+                continue      # no iteration points
             loops = [(v, c, c + 1) for v, c in w.task.env.items()]
             for v, lo, hi in task_loops:
                 if s >= 0 and plan.step_var is not None and v == plan.step_var.var:
@@ -791,7 +813,7 @@ class _Executor:
                 execute_chain(loops[len(w.task.env):], leaf, dict(w.task.env), plan.defs, read,
                               {plan.out_name: out_tile}, plugins, st, self.W.device(g))
             else:
-                run_leaf(policy, loops, leaf, plan.defs, out_tile, ins, st)
+                run_leaf(policy, loops, leaf, plan.defs, out_tile, ins, st, accumulate=acc)
 
     def release(self, s):
         for hid, last in self.prog.last_use.items():
@@ -805,9 +827,23 @@ class _Executor:
         for g in self.owned:
             self._sync(self.xstream(g), self.cstream(g))
         sends, recvs, staged = [], [], {}
+        tokens = []           # (inbox, writer token, home token) of peer-memory write-backs
         for k, c in enumerate(self.prog.commits):
             gt, gh = self.gpu(c.task.coord), self.gpu(c.home)
             if gt == gh:
+                continue
+            ib = self.inbox.get(c.task.coord)
+            if ib is not None:
+                # the partial is already in the home's inbox: an 8-byte token orders
+                # the home's accumulation after the writer's leaf
+                tw = self._token(gt) if self.W.owns(gt) else None
+                th = self._token(gh) if self.W.owns(gh) else None
+                if tw is not None:
+                    sends.append((gt, gh, tw))
+                if th is not None:
+                    recvs.append((gh, gt, th))
+                    staged[k] = ib.home_view()
+                tokens.append((ib, tw, th))
                 continue
             if self.W.owns(gt):
                 self.out_bufs[c.task.coord].record_stream(self.xstream(gt))
@@ -830,6 +866,28 @@ class _Executor:
         for g in self.owned:
             self._sync(self.cstream(g), self.xstream(g))
         self._apply_commits(region, [(c, staged.get(k)) for k, c in enumerate(self.prog.commits)])
+        if tokens:
+            # credit: the home has read its inboxes; the writers' next leaves may overwrite them
+            for g in self.owned:
+                self._sync(self.xstream(g), self.cstream(g))
+            sends, recvs = [], []
+            for ib, tw, th in tokens:
+                if th is not None:
+                    sends.append((ib.home_gpu, ib.writer_gpu, th))
+                if tw is not None:
+                    recvs.append((ib.writer_gpu, ib.home_gpu, tw))
+            self._nccl(sends, recvs)
+            for ib, tw, th in tokens:
+                if tw is not None:
+                    ev = self.torch.cuda.Event()
+                    ev.record(self.xstream(ib.writer_gpu))
+                    ib.credit = ev
+
+    def _token(self, g):
+        torch = self.torch
+        with torch.cuda.stream(self.xstream(g)):
+            t = torch.empty(1, dtype=torch.float64, device=self.W.device(g))
+        return t
 
 
 _PLAN_CACHE: dict = {}

@@ -65,6 +65,40 @@ def main():
         if not np.array_equal(res.output.data, np.asarray(want)):
             failures.append(f"oracle {b.name} {b.machine}")
 
+    # peer-memory write-backs: the leaf stores its partial into the home GPU's
+    # inbox (peer.py); bitwise equal to the NCCL write-back path, also when one
+    # program runs twice (inbox reuse behind the credit token)
+    from paper_2203_08069_b200 import peer
+    peer_cases = [td.cosma_like((1, 1, 2), (1, 1, 1), dims=(136, 120, 200))]
+    if size >= 4:
+        peer_cases.append(td.cosma_like((2, 1, 2), (1, 1, 1), dims=(130, 96, 150)))
+    if size >= 8:
+        peer_cases.append(td.johnson(2, 2, 2, dims=(128, 96, 160)))
+    for b in peer_cases:
+        got = {}
+        for flag in (True, False):
+            peer.PEER_REDUCE = flag
+            for mode in (0, 1):
+                cin, store = b.prepare(seed=5, mode=mode, world=world)
+                outs = []
+                for _ in range(2):
+                    store.zero(b.statement.lhs.tensor.name)
+                    td.execute(cin, store)
+                    outs.append(store[b.statement.lhs.tensor.name].tensor.data.copy())
+                got[(flag, mode)] = outs
+        peer.PEER_REDUCE = True
+        used = sum(len(s.inboxes) for s in world.inbox_sets.values())
+        for mode in (0, 1):
+            a, bb = got[(True, mode)], got[(False, mode)]
+            if not (np.array_equal(a[0], a[1]) and np.array_equal(a[0], bb[0]) and np.array_equal(bb[0], bb[1])):
+                failures.append(f"peer {b.name} {b.machine} mode {mode}")
+        ins = {n: generate(b.statement.tensors()[n].dims, 5, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = seq_eval(td.format_statement(b.statement), b.statement.extents, ins)
+        if not np.array_equal(got[(True, 0)][0], np.asarray(want)):
+            failures.append(f"peer oracle {b.name} {b.machine}")
+        if rank == 0:
+            print(f"peer {b.name} {b.machine}: inboxes in use {used}", flush=True)
+
     # placement-phase movement over NCCL
     machine = td.grid(2, 2)
     old = td.TensorDistribution((6, 8), machine, [(("x", "y"), ("x", 0))])

@@ -33,10 +33,27 @@ n = min(4, __import__('torch').cuda.device_count())
 td.configure(list(range(n)))
 for b in (td.summa(4, 1, dims=(64, 48, 80), chunk=16), td.cannon(2, 2, dims=(40, 36, 44)),
           td.johnson(2, 2, 2, dims=(24, 20, 28)), td.mttkrp(2, 2, dims=(12, 8, 10, 9)),
-          td.innerprod3(2, dims=(8, 6, 30))):
+          td.innerprod3(2, dims=(8, 6, 30)), td.cosma_like((1, 1, 2), (1, 1, 1), dims=(72, 56, 90))):
     res, ins = b.run(seed=2)
     want = seq_eval(td.format_statement(b.statement), b.statement.extents, {k: v.data for k, v in ins.items()})
     assert np.array_equal(res.output.data, np.asarray(want)), b.name
+# peer-memory write-back (cosma k-split): same bits as the NCCL path, twice in a row
+from paper_2203_08069_b200 import peer
+from oracle.generator import generate
+b = td.cosma_like((1, 1, 2), (1, 1, 1), dims=(200, 136, 264))
+res = {}
+for flag in (True, False):
+    peer.PEER_REDUCE = flag
+    cin, store = b.prepare(seed=4, mode=1, world=td.comm.world())
+    outs = []
+    for _ in range(2):
+        store.zero("A")
+        td.execute(cin, store)
+        outs.append(store["A"].tensor.data.copy())
+    res[flag] = outs
+peer.PEER_REDUCE = True
+assert all(np.array_equal(res[True][0], x) for x in res[True][1:] + res[False]), "peer vs nccl write-back"
+assert any(s.inboxes for s in td.comm.world().inbox_sets.values()), "peer inbox path not taken"
 print("single-process multi-gpu OK")
 """ % ROOT
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
