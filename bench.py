@@ -229,8 +229,10 @@ def bench_gemm(job, steps, warmup, e2e_steps):
     # parity spot check of the last step: exact on integer inputs (Freivalds-style row sample)
     check = _gemm_spot_check(job, store, bundle, n)
 
-    # per-launch roofline of the dominant kernel on this rank
-    flop_per_launch = _dgemm_flop_per_launch(bundle, n)
+    # roofline of the dominant kernel on this rank: the rank's algorithmic GEMM flop
+    # over the summed device time of its DMMA launches (the pipelined first step
+    # runs its k-range as two launches, so launches differ in size)
+    flop_per_launch = 2.0 * n ** 3 / p * steps / n_dgemm if n_dgemm else None
     achieved = flop_per_launch / (dgemm_ms / 1e3) / 1e12 if dgemm_ms else None
 
     # e2e through the public API with host buffers
@@ -252,19 +254,6 @@ def bench_gemm(job, steps, warmup, e2e_steps):
                      "flop_per_launch": flop_per_launch},
         "clocks": clk.summary(), "e2e": e2e, "overlap": overlap,
     }
-
-
-def _dgemm_flop_per_launch(bundle, n):
-    g = bundle.machine.flat_dims
-    if bundle.name == "cannon":
-        b = -(-n // g[0])
-        return 2.0 * b * b * b
-    if bundle.name == "johnson":
-        b = -(-n // g[0])
-        return 2.0 * b ** 3
-    if bundle.name == "summa":  # 2 x 1 grid, 8 k-chunks
-        return 2.0 * (-(-n // g[0])) * n * (-(-n // 8))
-    return 2.0 * n ** 3
 
 
 def _gemm_spot_check(job, store, bundle, n):

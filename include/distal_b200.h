@@ -156,6 +156,8 @@ int td_comm_destroy(void* comm);
 /* Sub-communicator over the ranks that pass the same color >= 0 (ranked by
  * key); color < 0 = not a member (*newcomm = NULL).  Collective over `comm`.
  * Used for the broadcast groups of fan-out transfers (SUMMA/COSMA panels). */
+/* Inside td_group_start/end (one thread splitting several communicators) NCCL
+ * writes *newcomm at td_group_end: keep the slot alive until then. */
 int td_comm_split(void* comm, int color, int key, void** newcomm);
 int td_group_start(void);
 int td_group_end(void);

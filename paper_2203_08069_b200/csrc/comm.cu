@@ -56,10 +56,11 @@ int td_comm_init_all(void** comms, int ndev, const int* devices) {
 
 int td_comm_split(void* comm, int color, int key, void** newcomm) {
   TD_REQUIRE(comm && newcomm, "comm_split: bad arguments");
-  ncclComm_t out = nullptr;
-  TD_NCCL(ncclCommSplit(static_cast<ncclComm_t>(comm), color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &out,
-                        nullptr));
-  *newcomm = out;
+  // inside ncclGroupStart/End (one thread splitting several communicators) NCCL
+  // fills the handle only at ncclGroupEnd: hand it the caller's slot, not a local
+  *newcomm = nullptr;
+  TD_NCCL(ncclCommSplit(static_cast<ncclComm_t>(comm), color < 0 ? NCCL_SPLIT_NOCOLOR : color, key,
+                        reinterpret_cast<ncclComm_t*>(newcomm), nullptr));
   return TD_OK;
 }
 

@@ -476,6 +476,37 @@ def _box_cached(loops, leaf, defs):
     return box
 
 
+def native_plan(policy: str, loops, leaf, defs):
+    """(Match, box) when this step nest runs as one native contraction over
+    the iteration box `box`, else None (nest kernel, empty box, plugins)."""
+    if not isinstance(leaf, Reduce) or policy in ("interpreter", "exact"):
+        return None
+    m = _classify_cached(leaf)
+    want = {"gemm": "dgemm"}.get(policy, policy)
+    if m is None or not (want == "auto" or want == m.kind):
+        return None
+    box = _box_cached(loops, leaf, defs)
+    if not box:
+        return None
+    return m, box
+
+
+def contracted_var(m, leaf):
+    """The summed statement variable of a native GEMM leaf (k of C(i,j) += A(i,k) B(k,j))."""
+    if m.kind != "dgemm":
+        return None
+    return accesses_of(leaf.rhs)[m.roles["A"]].var_names[1]
+
+
+def run_native_box(m, leaf, box, out: DeviceTile, ins, stream, accumulate: int = 1) -> None:
+    """Launch the native contraction `m` over `box` (a sub-box of the nest's
+    iteration box: the pipelined first step runs its k-range in pieces)."""
+    ev = _timing_start(stream)
+    if not _launch_native(m, leaf, box, out, ins, stream, accumulate):
+        raise TendistError(f"native {m.kind} leaf cannot address its operands on the box {box}")
+    _timing_stop(m.kind, ev, stream)
+
+
 def _zero_tile(out: DeviceTile, stream) -> None:
     """out = +0.0 on `stream` (contiguous tiles, including peer inboxes)."""
     data = out.data

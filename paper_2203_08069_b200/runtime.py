@@ -40,7 +40,7 @@ from .errors import (ConfigError, ExtentMismatch, MissingDistribution, MissingIn
                      VerifyFail)
 from .interp import DeviceTile, execute_chain, stream_handle, torch_mod
 from .ir import TensorIndexStmt, accesses_of
-from .leaves import BUILTIN_LEAVES, run_leaf
+from .leaves import BUILTIN_LEAVES, contracted_var, native_plan, run_leaf, run_native_box
 from .machine import Machine
 from .planner import build_program
 from .tensors import DenseTensor
@@ -52,6 +52,26 @@ USE_BROADCAST = True
 # issue step s+1's NCCL group while step s's leaves run (False serialises them: a
 # measurement switch for the overlap, used by bench.py)
 OVERLAP_COMM = True
+# pipeline the first step: its cross-GPU transfers go in two k-pieces (1/8, 7/8)
+# and the GEMM leaves start on the first piece while the rest is in flight
+# (nothing earlier can hide step 0's transfers: Cannon's skew, Johnson's faces)
+SPLIT_FIRST_STEP = True
+SPLIT_MIN_BYTES = 32 << 20
+
+
+def _k_cuts(lo: int, hi: int) -> list:
+    """Pieces of a k-range for the pipelined first step: a short head
+    (1/8, rounded up to 64) that arrives quickly, then the rest."""
+    n = hi - lo
+    head = min(n, -(-max(1, n // 8) // 64) * 64)
+    if n < 256 or head >= n:
+        return [(lo, hi)]
+    return [(lo, lo + head), (lo + head, hi)]
+
+
+def _with_range(rect: HyperRect, axis: int, lo: int, hi: int) -> HyperRect:
+    return HyperRect(tuple(lo if a == axis else x for a, x in enumerate(rect.lo)),
+                     tuple(hi if a == axis else x for a, x in enumerate(rect.hi)))
 
 
 def _strides(t):
@@ -540,6 +560,11 @@ class _Executor:
                 if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
                     for g in self.owned:
                         self._sync(self.xstream(g), self.cstream(g))
+                split = self._split_plan(s) if s == 0 and self.prog.stepwise else None
+                if split is not None:
+                    self.compute_split(self.prog.work[s], s, split, self.transfers_split(self.prog.transfers[s], split))
+                    self.release(s)
+                    continue
                 self.transfers(self.prog.transfers[s])
                 for g in self.owned:
                     self._sync(self.cstream(g), self.xstream(g))
@@ -668,16 +693,17 @@ class _Executor:
         for wave in sorted({t.wave for t in moves}):
             self._transfer_group([t for t in moves if t.wave == wave])
 
-    def _send_view(self, gs, t):
-        """Contiguous device view of a transfer's part on its source GPU."""
+    def _send_view(self, gs, t, part=None):
+        """Contiguous device view of a transfer's part (or a sub-box of it) on its source GPU."""
         torch = self.torch
+        part = t.part if part is None else part
         src_h = self.prog.holdings[t.src_hid]
-        self.wait_piece(self.xstream(gs), t.src_hid, t.part)
-        view = _slice(self.holding_buf(t.src_hid), src_h.rect, t.part)
+        self.wait_piece(self.xstream(gs), t.src_hid, part)
+        view = _slice(self.holding_buf(t.src_hid), src_h.rect, part)
         if not view.is_contiguous():
             st = self.xstream(gs)
             with torch.cuda.stream(st):
-                packed = torch.empty(t.part.shape, dtype=torch.float64, device=view.device)
+                packed = torch.empty(part.shape, dtype=torch.float64, device=view.device)
             _copy_box(st, packed, view)
             view = packed
         return view
@@ -778,6 +804,144 @@ class _Executor:
                 continue
             _copy_box(st, _slice(buf, rect, part), _slice(self.holding_buf(hid), h.rect, part))
         return buf
+
+    # ---- pipelined first step
+    def _work_loops(self, w, s, task_loops):
+        plan = self.plan
+        loops = [(v, c, c + 1) for v, c in w.task.env.items()]
+        for v, lo, hi in task_loops:
+            if s >= 0 and plan.step_var is not None and v == plan.step_var.var:
+                lo, hi = s, s + 1
+            loops.append((v, lo, hi))
+        return loops
+
+    def _split_plan(self, s):
+        """{"kv", "axis": {tensor: axis}} when step s may run pipelined, else None.
+
+        Decided from the program alone (identical on every rank: it shapes the
+        NCCL groups): every leaf of the step is a native GEMM over its whole
+        iteration box, every cross-GPU transfer is a single-destination p2p
+        move of an operand along whose k axis the receiving task's box spans
+        exactly the transferred range, and enough bytes move to matter."""
+        if not (SPLIT_FIRST_STEP and self.W.multi_gpu):
+            return None
+        moves = self.prog.transfers[s]
+        cross = [t for t in moves if self.gpu(t.src) != self.gpu(t.dst)]
+        if not cross or any(t.wave for t in moves):
+            return None
+        if 8 * max(t.part.volume for t in cross) < SPLIT_MIN_BYTES:
+            return None
+        fan = {}
+        for t in cross:
+            fan.setdefault((self.gpu(t.src), t.src_hid, t.part), set()).add(self.gpu(t.dst))
+        if self.use_bcast and any(len(d) >= 2 for d in fan.values()):
+            return None
+        plan = self.plan
+        task_loops, leaf = _loops_of(plan.task_body)
+        policy, plugins = _leaf_choice(plan.relations, [v for v, _, _ in task_loops], self.policy)
+        if plugins:
+            return None
+        rhs = accesses_of(leaf.rhs)
+        dst_of = {t.dst_hid: t for t in cross}
+        kv, axis = None, {}
+        for w in self.prog.work[s]:
+            np_ = native_plan(policy, self._work_loops(w, s, task_loops), leaf, plan.defs)
+            if np_ is None:
+                return None
+            m, box = np_
+            k = contracted_var(m, leaf)
+            if k is None or (kv is not None and k != kv):
+                return None
+            kv = k
+            for a in rhs:
+                if kv in a.var_names:
+                    axis[a.tensor.name] = a.var_names.index(kv)
+            for key, (name, rect, hids) in w.operands.items():
+                fed = [h for h in hids if h in dst_of]
+                if not fed:
+                    continue
+                if len(hids) != 1 or rect is None or name not in axis:
+                    return None
+                ax = axis[name]
+                t = dst_of[hids[0]]
+                if (rect.lo[ax], rect.hi[ax]) != box[kv] or (t.part.lo[ax], t.part.hi[ax]) != box[kv]:
+                    return None
+        if kv is None or any(t.tensor not in axis for t in cross):
+            return None
+        return {"kv": kv, "axis": axis}
+
+    def transfers_split(self, moves, split):
+        """Step-0 transfers in k-pieces: one NCCL group per piece, an event per
+        owned GPU after each.  Column pieces of row-major tiles are packed on
+        the sender and unpacked on the receiver by strided copies."""
+        torch = self.torch
+        cross = [t for t in moves if self.gpu(t.src) != self.gpu(t.dst)]
+        self._transfer_group([t for t in moves if self.gpu(t.src) == self.gpu(t.dst)])   # aliases
+        full = {}
+        for t in cross:
+            gd = self.gpu(t.dst)
+            if self.W.owns(gd):
+                full[t.dst_hid] = self.buffers[t.dst_hid] = self._recv_buf(gd, t.part)
+        npieces = max(len(_k_cuts(t.part.lo[split["axis"][t.tensor]], t.part.hi[split["axis"][t.tensor]]))
+                      for t in cross)
+        events = {g: [] for g in self.owned}
+        for c in range(npieces):
+            sends, recvs, unpack = [], [], []
+            for t in cross:
+                ax = split["axis"][t.tensor]
+                cuts = _k_cuts(t.part.lo[ax], t.part.hi[ax])
+                if c >= len(cuts):
+                    continue
+                sub = _with_range(t.part, ax, *cuts[c])
+                gs, gd = self.gpu(t.src), self.gpu(t.dst)
+                if self.W.owns(gs):
+                    sends.append((gs, gd, self._send_view(gs, t, sub)))
+                if self.W.owns(gd):
+                    dst = _slice(full[t.dst_hid], t.part, sub)
+                    if not dst.is_contiguous():
+                        with torch.cuda.stream(self.xstream(gd)):
+                            stage = torch.empty(sub.shape, dtype=torch.float64, device=self.W.device(gd))
+                        unpack.append((gd, dst, stage))
+                        dst = stage
+                    recvs.append((gd, gs, dst))
+            self._nccl(sends, recvs)
+            for gd, dst, stage in unpack:
+                _copy_box(self.xstream(gd), dst, stage)
+            for g in self.owned:
+                ev = torch.cuda.Event()
+                ev.record(self.xstream(g))
+                events[g].append(ev)
+        return events
+
+    def compute_split(self, works, s, split, events):
+        """Step-0 GEMM leaves in the k-pieces of `transfers_split`: piece c
+        waits only for the transfers of pieces <= c."""
+        plan = self.plan
+        task_loops, leaf = _loops_of(plan.task_body)
+        policy, _ = _leaf_choice(plan.relations, [v for v, _, _ in task_loops], self.policy)
+        rhs = accesses_of(leaf.rhs)
+        kv = split["kv"]
+        for w in works:
+            g = self.gpu(w.task.coord)
+            if not self.W.owns(g) or w.task.out_rect is None:
+                continue
+            st = self.cstream(g)
+            st.wait_event(events[g][0])
+            acc = 0 if w.task.coord in self.inbox else 1
+            m, box = native_plan(policy, self._work_loops(w, s, task_loops), leaf, plan.defs)
+            out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
+                                  plan.out_access.tensor.dims)
+            tiles = {key: DeviceTile(name, rect, self.operand(g, name, rect, hids), self.store[name].dims)
+                     for key, (name, rect, hids) in w.operands.items()}
+            ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
+            for c, (a, b) in enumerate(_k_cuts(*box[kv])):
+                if c:
+                    st.wait_event(events[g][min(c, len(events[g]) - 1)])
+                sub = dict(box)
+                sub[kv] = (a, b)
+                run_native_box(m, leaf, sub, out_tile, ins, st, acc if c == 0 else 1)
+            for e in events[g][1:]:
+                st.wait_event(e)
 
     def compute(self, works, s):
         plan = self.plan

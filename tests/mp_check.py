@@ -65,6 +65,21 @@ def main():
         if not np.array_equal(res.output.data, np.asarray(want)):
             failures.append(f"oracle {b.name} {b.machine}")
 
+    # pipelined first step (k-pieces on the transfers and the GEMM leaves), forced on at test sizes
+    from paper_2203_08069_b200 import runtime as rt
+    saved = rt.SPLIT_MIN_BYTES
+    rt.SPLIT_MIN_BYTES = 0
+    for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.johnson(2, 2, 2, dims=(264, 200, 1040)),
+              td.summa(2, 1, dims=(200, 160, 2048), chunk=512),
+              td.cosma_like((1, 1, 2), (1, 1, 1), dims=(136, 120, 1200))):
+        for seed in (9, 10):
+            res, ins = b.run(seed=seed)
+            want = seq_eval(td.format_statement(b.statement), b.statement.extents,
+                            {n: t.data for n, t in ins.items()})
+            if not np.array_equal(res.output.data, np.asarray(want)):
+                failures.append(f"split {b.name} {b.machine} seed {seed}")
+    rt.SPLIT_MIN_BYTES = saved
+
     # peer-memory write-backs: the leaf stores its partial into the home GPU's
     # inbox (peer.py); bitwise equal to the NCCL write-back path, also when one
     # program runs twice (inbox reuse behind the credit token)

@@ -37,6 +37,14 @@ for b in (td.summa(4, 1, dims=(64, 48, 80), chunk=16), td.cannon(2, 2, dims=(40,
     res, ins = b.run(seed=2)
     want = seq_eval(td.format_statement(b.statement), b.statement.extents, {k: v.data for k, v in ins.items()})
     assert np.array_equal(res.output.data, np.asarray(want)), b.name
+# pipelined first step, forced on at test sizes
+from paper_2203_08069_b200 import runtime as rt
+rt.SPLIT_MIN_BYTES = 0
+for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.johnson(2, 2, 2, dims=(264, 200, 1040))):
+    res, ins = b.run(seed=9)
+    want = seq_eval(td.format_statement(b.statement), b.statement.extents, {k: v.data for k, v in ins.items()})
+    assert np.array_equal(res.output.data, np.asarray(want)), "split " + b.name
+rt.SPLIT_MIN_BYTES = 32 << 20
 # peer-memory write-back (cosma k-split): same bits as the NCCL path, twice in a row
 from paper_2203_08069_b200 import peer
 from oracle.generator import generate

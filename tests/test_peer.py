@@ -53,3 +53,44 @@ def test_cosma_k_split_qualifies_and_multi_step_does_not():
                                     td.ttv(4, dims=(8, 4, 6))])
 def test_no_cross_gpu_reduction_no_inbox(bundle):
     assert _eligible(bundle, bundle.machine.size)[1] == {}
+
+
+# ---- pipelined first step (runtime._split_plan / _k_cuts), host side
+class _FakeWorld:
+    def __init__(self, ngpus):
+        self.ngpus = ngpus
+        self.multi_gpu = ngpus > 1
+
+
+def _executor(bundle, ngpus, policy="auto"):
+    from paper_2203_08069_b200.runtime import _Executor
+    prog, _ = plan_statement(bundle.statement, bundle.machine, bundle.distributions, bundle.schedule)
+    ex = object.__new__(_Executor)
+    ex.prog, ex.plan, ex.W, ex.m, ex.policy, ex.use_bcast = prog, prog.plan, _FakeWorld(ngpus), bundle.machine, \
+        policy, True
+    return ex
+
+
+def test_k_cuts():
+    from paper_2203_08069_b200.runtime import _k_cuts
+    assert _k_cuts(0, 13056) == [(0, 1664), (1664, 13056)]
+    assert _k_cuts(100, 300) == [(100, 300)]          # too short to split
+    cuts = _k_cuts(5, 16389)
+    assert cuts[0][0] == 5 and cuts[-1][1] == 16389 and (cuts[0][1] - 5) % 64 == 0
+
+
+@pytest.mark.parametrize("bundle,ngpus", [(td.cannon(2, 2, dims=(4096, 4096, 4096)), 4),
+                                          (td.johnson(2, 2, 2, dims=(4096, 4096, 4096)), 8),
+                                          (td.johnson(2, 2, 2, dims=(4096, 4096, 4096)), 4)])
+def test_first_step_pipelines_for_the_gemm_sweeps(bundle, ngpus):
+    split = _executor(bundle, ngpus)._split_plan(0)
+    assert split == {"kv": "k", "axis": {"A": 1, "B": 0}}
+
+
+def test_first_step_stays_whole_when_it_must():
+    # the exact policy (nest kernel), small transfers, single GPU
+    assert _executor(td.cannon(2, 2, dims=(4096,) * 3), 4, policy="exact")._split_plan(0) is None
+    assert _executor(td.cannon(2, 2, dims=(256,) * 3), 4)._split_plan(0) is None
+    assert _executor(td.cannon(2, 2, dims=(4096,) * 3), 1)._split_plan(0) is None
+    # MTTKRP is not a GEMM leaf
+    assert _executor(td.mttkrp(2, 2, dims=(512, 32, 512, 512)), 4)._split_plan(0) is None
