@@ -78,6 +78,17 @@ def main():
                             {n: t.data for n, t in ins.items()})
             if not np.array_equal(res.output.data, np.asarray(want)):
                 failures.append(f"split {b.name} {b.machine} seed {seed}")
+    if size >= 4:
+        # split first step + peer inboxes together (Johnson 2x2x2 at 8 GPUs does both), twice in a row
+        b = td.cosma_like((2, 1, 2), (1, 1, 1), dims=(130, 96, 1200))
+        cin, store = b.prepare(seed=6, mode=0, world=world)
+        ins = {n: generate(b.statement.tensors()[n].dims, 6, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+        for rep in range(2):
+            store.zero("A")
+            td.execute(cin, store)
+            if not np.array_equal(store["A"].tensor.data, want):
+                failures.append(f"split+peer {b.machine} rep {rep}")
     rt.SPLIT_MIN_BYTES = saved
 
     # peer-memory write-backs: the leaf stores its partial into the home GPU's
