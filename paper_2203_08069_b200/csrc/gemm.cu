@@ -466,33 +466,9 @@ int dgemm_rowsum_tile_rows(int config) {
   }
 }
 
-int dgemm_rowsum_slots(int config, int* bm, int* bn) {
-  int dev = 0, sms = 0, per_sm = 0;
-  TD_CUDA(cudaGetDevice(&dev));
-  TD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  switch (config) {
-#define TD_ROWSUM_SLOTS_CASE(id, BM, BN, BK, WM, WN, ST, MINB)                                       \
-  case id: {                                                                                        \
-    using Cfg = TmaCfg<BM, BN, BK, WM, WN, ST, MINB>;                                               \
-    auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, ST, 1, MINB>;                                  \
-    TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES)); \
-    TD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM_BYTES)); \
-    *bm = BM;                                                                                       \
-    *bn = BN;                                                                                       \
-    return per_sm * sms;                                                                            \
-  }
-    TD_GEMM_TMA_CONFIGS(TD_ROWSUM_SLOTS_CASE)
-#undef TD_ROWSUM_SLOTS_CASE
-    default:
-      return 0;  // not a TMA config: no tail split
-  }
-}
-
-int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a, int64_t* split_used) {
+int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
   const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                     (batch == 1 || a.sA % 2 == 0);
-  if (batch + a.split_n > 65535 || a.split_n < 0 || a.split_n > batch || !tma_ok(batch, a)) a.split_n = 0;
-  if (split_used) *split_used = a.split_n;
   for (int64_t done = 0; done < batch;) {  // grid.y is limited to 65535
     const int64_t chunk = std::min<int64_t>(batch - done, 65535);
     GemmArgs c = a;
@@ -549,14 +525,14 @@ extern "C" {
 int td_dgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
              const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0, 0, nullptr, 0};
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a);
 }
 
 int td_dgemm_config(void* stream, int config, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0, 0, nullptr, 0};
+  td::GemmArgs a{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, accumulate, 0, 0, 0, nullptr, 0};
   return td::dgemm_dispatch(td::as_stream(stream), 1, a, config);
 }
 
@@ -564,7 +540,7 @@ int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t 
                      int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
                      double* C, int64_t ldc, int64_t strideC, int accumulate) {
   td::StreamDevice sd(stream);
-  td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0, 0, nullptr, 0, 0, nullptr, 0};
+  td::GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, accumulate, 0, 0, 0, nullptr, 0};
   int64_t done = 0;
   while (done < batch) {  // grid.y is limited to 65535
     const int64_t chunk = std::min<int64_t>(batch - done, 65535);

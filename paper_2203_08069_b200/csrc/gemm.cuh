@@ -22,21 +22,10 @@ struct GemmArgs {
   // of H(r, n) * (A.B)(r, n) -- one partial per M-tile, C is the workspace
   const double* H;
   int64_t ldh;
-  // EPI = 1 tail split (TMA body): the last `split_n` batches run as two CTAs
-  // each, over the two halves of the k-tile range, launched last (grid.y =
-  // batch + split_n) so the partial final wave is made of half-length CTAs;
-  // the second half's row sums go to C2[b - (batch - split_n)] (stride sC2)
-  int64_t split_n;
-  double* C2;
-  int64_t sC2;
 };
 
 // MTTKRP row-sum GEMMs (EPI = 1 in gemm.cu): rows per M-tile of a config, launch
 int dgemm_rowsum_tile_rows(int config);
-// *split_used = the tail split actually launched (a.split_n, or 0 when the
-// operands take the LDGSTS body or the batch needs several launches)
-int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a, int64_t* split_used);
-// resident CTAs per device of a row-sum config's TMA kernel and its tile shape
-int dgemm_rowsum_slots(int config, int* bm, int* bn);
+int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a);
 
 }  // namespace td

@@ -84,35 +84,17 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int tn = in_g / gsize;
   const int m0 = tm * BM;
   const int n0 = tn * BN;
-  int bz = blockIdx.y;
+  const int bz = blockIdx.y;
+  const int bzB = p.sB ? bz : 0;
   double* __restrict__ C = p.C + int64_t(bz) * p.sC;
   const int64_t M = p.M, N = p.N, K = p.K;
-  int kt0 = 0, kt1 = (int)ceil_div(K, BK);
-  if constexpr (EPI == 1) {  // tail split: the last split_n batches in two k-halves
-    const int nfull = (int)gridDim.y - 2 * (int)p.split_n;
-    if (bz >= nfull) {
-      const int r = bz - nfull;
-      const int h = r / (int)p.split_n;
-      const int q = r - h * (int)p.split_n;
-      bz = nfull + q;
-      const int mid = kt1 / 2;
-      if (h) {
-        kt0 = mid;
-        C = p.C2 + int64_t(q) * p.sC2;
-      } else {
-        kt1 = mid;
-        C = p.C + int64_t(bz) * p.sC;
-      }
-    }
-  }
-  const int bzB = p.sB ? bz : 0;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int wm0 = (warp / Cfg::WARPS_N) * WM;
   const int wn0 = (warp % Cfg::WARPS_N) * WN;
-  const int ktiles = kt1 - kt0;
+  const int ktiles = (int)ceil_div(K, BK);
 
   if (tid == 0) {
 #pragma unroll
@@ -121,9 +103,8 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
   __syncthreads();
 
-  auto issue = [&](int j) {  // j-th k-tile of this CTA's range
-    const int s = j % STAGES;
-    const int kt = kt0 + j;
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
     mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
     tma_load_4d(As + s * Cfg::A_STAGE, &tmA, 0, m0, kt * (BK / 4), bz, &full[s]);
     tma_load_4d(Bs + s * Cfg::B_STAGE, &tmB, 0, kt * BK, n0 / 4, bzB, &full[s]);

@@ -27,7 +27,6 @@
 // workspace; mttkrp_reduce finishes.  Measured 34.8 (TMA-fed body) and 33.4
 // (LDGSTS body) vs 30.9 TFLOP/s for the best fused configuration.
 #include "common.cuh"
-#include <cstdlib>
 #include "dmma.cuh"
 #include "gemm.cuh"
 
@@ -244,20 +243,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) mttkrp_kernel(MttkrpArgs p) 
 }
 
 // A(i, j) (+)= sum over the CTA groups of row i, ascending (fixed order)
-// work2 / split_n: rows i >= I - split_n also have second-half partials
-// (tail split of the row-sum GEMM), added after the first halves in group order
 __global__ void mttkrp_reduce(const double* __restrict__ work, int groups, int64_t I, int64_t R, double* A,
-                              int64_t lda, int accumulate, const double* __restrict__ work2 = nullptr,
-                              int64_t split_n = 0) {
+                              int64_t lda, int accumulate) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < I * R; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / R, j = e - (e / R) * R;
     const double* w = work + i * groups * R + j;
     double v = 0.0;
     for (int g = 0; g < groups; ++g) v += w[int64_t(g) * R];
-    if (i >= I - split_n) {
-      const double* w2 = work2 + (i - (I - split_n)) * groups * R + j;
-      for (int g = 0; g < groups; ++g) v += w2[int64_t(g) * R];
-    }
     double* dst = A + i * lda + j;
     *dst = accumulate ? *dst + v : v;
   }
@@ -317,25 +309,9 @@ static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
   const int bm = dgemm_rowsum_tile_rows(gemm_config);
   TD_REQUIRE(bm > 0, "mttkrp: unknown GEMM row-sum config %d", gemm_config);
   a.groups = (int)std::max<int64_t>(1, ceil_div(a.K, bm));
-  // tail split: when the CTAs' last wave would be at most half full, its tiles
-  // run as two half-k CTAs each (one half-length wave instead of a full one)
-  static const bool no_split = std::getenv("TD_NO_TAIL_SPLIT") != nullptr;  // measurement switch
-  int64_t split_n = 0;
-  if (!no_split && a.K > 0 && a.L >= 128) {
-    int sbm = 0, sbn = 0;
-    const int slots = dgemm_rowsum_slots(gemm_config, &sbm, &sbn);
-    if (slots > 0) {
-      const int64_t per_batch = ceil_div(a.K, sbm) * ceil_div(a.R, sbn);
-      const int64_t rem = (per_batch * a.I) % slots;
-      if (rem > 0 && 2 * rem <= slots) split_n = std::min<int64_t>(a.I, ceil_div(rem, per_batch));
-    }
-  }
-  const int64_t wsize = a.I * a.groups * a.R;
   if (int rc = retain_pool()) return rc;
-  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * (wsize + split_n * a.groups * a.R),
-                          st));
+  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * a.groups * a.R, st));
   int rc = TD_OK;
-  int64_t split_used = 0;
   if (a.K > 0 && a.L > 0) {
     GemmArgs g{};
     g.M = a.K; g.N = a.R; g.K = a.L;
@@ -343,16 +319,14 @@ static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
     g.B = a.D; g.ldb = a.ldd; g.sB = 0;
     g.C = a.work; g.ldc = a.R; g.sC = int64_t(a.groups) * a.R;
     g.H = a.C; g.ldh = a.ldc;
-    g.split_n = split_n; g.C2 = a.work + wsize; g.sC2 = int64_t(a.groups) * a.R;
-    rc = dgemm_rowsum(st, gemm_config, a.I, g, &split_used);
+    rc = dgemm_rowsum(st, gemm_config, a.I, g);
   } else {
-    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * wsize, st));
+    TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.groups * a.R, st));
   }
   if (rc == TD_OK) {
     const int64_t outs = a.I * a.R;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(outs, 256), 148 * 8));
-    mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, a.groups, a.I, a.R, a.A, a.lda, a.accumulate, a.work + wsize,
-                                          split_used);
+    mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, a.groups, a.I, a.R, a.A, a.lda, a.accumulate);
     rc = check_launch("mttkrp_reduce");
   }
   TD_CUDA(cudaFreeAsync(a.work, st));
