@@ -331,19 +331,32 @@ def bench_gemm_e2e(job, bundle, cin, steps):
                 for color, _ in s2.local_colors(bundle.distributions[name]):
                     s2.upload(name, color, slabs=nslabs[name], axis=slab_axis[name], copy_stream=k)
         s2.place_zeros(out, out_dist)
+        # p > 1: every output piece is final only after the last step, so that step's
+        # leaves run in row pieces and each piece's rows download as soon as they are done
+        s2.stream_rows = 4 if job.world.ngpus > 1 else 0
         td.execute(cin, s2, record_requirements=False)
         nbytes = 0
         for color, box, _ in out_dist.pieces():
             gpus = s2[out].gpus_of(color)
             if gpus and job.world.owns(gpus[0]):
-                ev = s2.done.get((out, gpus[0], color))
-                if ev is not None:
-                    d2h_stream.wait_event(ev)
-                else:
-                    d2h_stream.wait_stream(torch.cuda.current_stream(job.device))
                 piece = s2[out].piece(gpus[0], color)
-                with torch.cuda.stream(d2h_stream):
-                    sink[color].copy_(piece, non_blocking=True)
+                rows = s2.row_done.get((out, gpus[0], color))
+                if rows:
+                    for lo, hi, ev in rows:
+                        d2h_stream.wait_event(ev)
+                        with torch.cuda.stream(d2h_stream):
+                            sink[color][lo:hi].copy_(piece[lo:hi], non_blocking=True)
+                    ev = s2.done.get((out, gpus[0], color))
+                    if ev is not None:
+                        d2h_stream.wait_event(ev)
+                else:
+                    ev = s2.done.get((out, gpus[0], color))
+                    if ev is not None:
+                        d2h_stream.wait_event(ev)
+                    else:
+                        d2h_stream.wait_stream(torch.cuda.current_stream(job.device))
+                    with torch.cuda.stream(d2h_stream):
+                        sink[color].copy_(piece, non_blocking=True)
                 piece.record_stream(d2h_stream)
                 nbytes += box.volume * 8
         d2h_stream.synchronize()

@@ -151,6 +151,12 @@ class RegionStore:
         self.ready: dict = {}     # (tensor, gpu, color) -> [(box, CUDA event)] of slabs still arriving
         self.done: dict = {}      # (tensor, gpu, color) -> CUDA event after the last write of a launch
         self.pending: dict = {}   # (tensor, gpu, color) -> [box, buf, host, slabs left] deferred uploads
+        # output streaming (e2e): the last step's GEMM leaves of a directly written
+        # home piece run in `stream_rows` row pieces, each followed by an event in
+        # row_done[(tensor, gpu, color)] = [(row lo, row hi, event)] (piece-local rows),
+        # so a caller can start the D2H of finished rows while later rows compute
+        self.stream_rows: int = 0
+        self.row_done: dict = {}
 
     def __contains__(self, name) -> bool:
         return name in self.regions
@@ -534,6 +540,7 @@ class _Executor:
             self._sync(self.cstream(g), cur)
             self._sync(self.xstream(g), cur)
         out_region = self.store[self.plan.out_name]
+        self.store.row_done = {k: v for k, v in self.store.row_done.items() if k[0] != self.plan.out_name}
         self.direct = self._direct_commits(out_region)
         self.inbox = self._inboxes()
         for t in self.plan.tasks:
@@ -972,12 +979,47 @@ class _Executor:
                 tiles[key] = DeviceTile(name, rect, self.operand(g, name, rect, hids),
                                         self.store[name].dims)
             ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
+            if not plugins and acc and self._stream_rows(w, s, g, loops, leaf, policy, out_tile, ins, st):
+                continue
             if plugins:
                 read = {a.tensor.name: tiles[(a.tensor.name, a.var_names)] for a in rhs}
                 execute_chain(loops[len(w.task.env):], leaf, dict(w.task.env), plan.defs, read,
                               {plan.out_name: out_tile}, plugins, st, self.W.device(g))
             else:
                 run_leaf(policy, loops, leaf, plan.defs, out_tile, ins, st, accumulate=acc)
+
+    def _stream_rows(self, w, s, g, loops, leaf, policy, out_tile, ins, st) -> bool:
+        """Last step of a task that writes its home piece directly (and alone):
+        run the native GEMM leaf in row pieces with an event after each
+        (RegionStore.stream_rows / row_done).  False: not applicable."""
+        n = self.store.stream_rows
+        if n < 2 or s != self.plan.num_steps - 1 or w.task.coord not in self.direct:
+            return False
+        color = self.direct[w.task.coord]
+        if sum(1 for c in self.prog.commits if self.gpu(c.home) == g and c.color == color) != 1:
+            return False
+        np_ = native_plan(policy, loops, leaf, self.plan.defs)
+        if np_ is None or contracted_var(np_[0], leaf) is None:
+            return False
+        m, box = np_
+        rv = leaf.lhs.var_names[0]
+        lo, hi = box[rv]
+        step = -(-max(1, (hi - lo) // n) // 64) * 64
+        if hi - lo < 2 * step:
+            return False
+        key = (self.plan.out_name, g, color)
+        base = out_tile.rect.lo[0]
+        marks = []
+        for a in range(lo, hi, step):
+            b = min(hi, a + step)
+            sub = dict(box)
+            sub[rv] = (a, b)
+            run_native_box(m, leaf, sub, out_tile, ins, st, 1)
+            ev = self.torch.cuda.Event()
+            ev.record(st)
+            marks.append((a - base, b - base, ev))
+        self.store.row_done[key] = marks
+        return True
 
     def release(self, s):
         for hid, last in self.prog.last_use.items():

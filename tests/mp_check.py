@@ -91,6 +91,19 @@ def main():
                 failures.append(f"split+peer {b.machine} rep {rep}")
     rt.SPLIT_MIN_BYTES = saved
 
+    # output streaming: the last step's leaves in row pieces with per-piece events (e2e D2H overlap)
+    for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.summa(2, 1, dims=(600, 160, 512), chunk=128)):
+        cin, store = b.prepare(seed=8, mode=0, world=world)
+        store.stream_rows = 4
+        td.execute(cin, store)
+        out = b.statement.lhs.tensor.name
+        ins = {n: generate(b.statement.tensors()[n].dims, 8, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+        if not store.row_done or any(len(v) < 2 for v in store.row_done.values()):
+            failures.append(f"stream rows {b.name}: no row pieces")
+        if not np.array_equal(store[out].tensor.data, want):
+            failures.append(f"stream rows {b.name} values")
+
     # peer-memory write-backs: the leaf stores its partial into the home GPU's
     # inbox (peer.py); bitwise equal to the NCCL write-back path, also when one
     # program runs twice (inbox reuse behind the credit token)
