@@ -331,9 +331,10 @@ def bench_gemm_e2e(job, bundle, cin, steps):
                 for color, _ in s2.local_colors(bundle.distributions[name]):
                     s2.upload(name, color, slabs=nslabs[name], axis=slab_axis[name], copy_stream=k)
         s2.place_zeros(out, out_dist)
-        # p > 1: every output piece is final only after the last step, so that step's
-        # leaves run in row pieces and each piece's rows download as soon as they are done
-        s2.stream_rows = 4 if job.world.ngpus > 1 else 0
+        # the last step's leaves of each output piece run in row pieces and each piece's
+        # rows download as soon as they are done (at p > 1 every output piece is final
+        # only after the last step; at p = 1 this shortens the last row block's tail)
+        s2.stream_rows = 4
         td.execute(cin, s2, record_requirements=False)
         nbytes = 0
         for color, box, _ in out_dist.pieces():
