@@ -335,6 +335,8 @@ def bench_gemm_e2e(job, bundle, cin, steps):
         # rows download as soon as they are done (at p > 1 every output piece is final
         # only after the last step; at p = 1 this shortens the last row block's tail)
         s2.stream_rows = 4
+        # p > 1: the pipelined first step moves and multiplies k in the A upload's 8 slabs
+        s2.first_step_pieces = nslabs["A"]
         td.execute(cin, s2, record_requirements=False)
         nbytes = 0
         for color, box, _ in out_dist.pieces():
@@ -371,10 +373,22 @@ def bench_gemm_e2e(job, bundle, cin, steps):
         step()
     job.barrier()
     dt = job.max_over_ranks(time.perf_counter() - t0)
+    # the downloaded output of the last e2e step: sampled rows exact (integer inputs)
+    n = bundle.statement.extents["i"]
+    ok = True
+    for color, box, _ in out_dist.pieces():
+        if color not in sink:
+            continue
+        w = min(64, box.hi[1] - box.lo[1])
+        b_cols = generate_box((n, n), (0, box.lo[1]), (n, w), 0, 2, 0)
+        for r in (box.lo[0], (box.lo[0] + box.hi[0]) // 2, box.hi[0] - 1):
+            a_row = generate_box((n, n), (r, 0), (1, n), 0, 1, 0)
+            ok = ok and bool(np.array_equal(sink[color][r - box.lo[0], :w].numpy(), (a_row @ b_cols).ravel()))
+    ok = job.sum_over_ranks(0.0 if ok else 1.0) == 0.0
     flop = 2.0 * bundle.statement.extents["i"] * bundle.statement.extents["j"] * bundle.statement.extents["k"]
     return {"value": flop * steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(job.sum_over_ranks(h2d)),
             "d2h_bytes_per_step": int(job.sum_over_ranks(d2h)), "ms_per_step": dt * 1e3 / steps,
-            "steps": steps, "algorithm": f"{bundle.name} {bundle.machine}",
+            "steps": steps, "algorithm": f"{bundle.name} {bundle.machine}", "rows_exact": ok,
             "how": "pinned host pieces -> RegionStore.place_local (async H2D in k-slabs on two copy streams, "
                    "overlapped with the leaves of earlier k-chunks) -> execute -> D2H of each home output "
                    "piece as soon as it is final (store.done events); host wall clock, max over ranks"}

@@ -59,10 +59,14 @@ SPLIT_FIRST_STEP = True
 SPLIT_MIN_BYTES = 32 << 20
 
 
-def _k_cuts(lo: int, hi: int) -> list:
+def _k_cuts(lo: int, hi: int, pieces: int = 2) -> list:
     """Pieces of a k-range for the pipelined first step: a short head
-    (1/8, rounded up to 64) that arrives quickly, then the rest."""
+    (1/8, rounded up to 64) that arrives quickly, then the rest; or, with
+    pieces > 2 (inputs still uploading, RegionStore.first_step_pieces),
+    `pieces` equal parts cut like the upload slabs (RegionStore.upload)."""
     n = hi - lo
+    if pieces > 2 and n >= 64 * pieces:
+        return [(lo + (q * n) // pieces, lo + ((q + 1) * n) // pieces) for q in range(pieces)]
     head = min(n, -(-max(1, n // 8) // 64) * 64)
     if n < 256 or head >= n:
         return [(lo, hi)]
@@ -157,6 +161,11 @@ class RegionStore:
         # so a caller can start the D2H of finished rows while later rows compute
         self.stream_rows: int = 0
         self.row_done: dict = {}
+        # k-pieces of the pipelined first step (runtime._k_cuts): 2 = head + rest;
+        # with inputs uploading in k-slabs, set it to the slab count so every piece
+        # waits only for its own slabs.  Must be equal on every rank (it shapes the
+        # NCCL groups).
+        self.first_step_pieces: int = 2
 
     def __contains__(self, name) -> bool:
         return name in self.regions
@@ -889,14 +898,15 @@ class _Executor:
             gd = self.gpu(t.dst)
             if self.W.owns(gd):
                 full[t.dst_hid] = self.buffers[t.dst_hid] = self._recv_buf(gd, t.part)
-        npieces = max(len(_k_cuts(t.part.lo[split["axis"][t.tensor]], t.part.hi[split["axis"][t.tensor]]))
+        kp = self.store.first_step_pieces
+        npieces = max(len(_k_cuts(t.part.lo[split["axis"][t.tensor]], t.part.hi[split["axis"][t.tensor]], kp))
                       for t in cross)
         events = {g: [] for g in self.owned}
         for c in range(npieces):
             sends, recvs, unpack = [], [], []
             for t in cross:
                 ax = split["axis"][t.tensor]
-                cuts = _k_cuts(t.part.lo[ax], t.part.hi[ax])
+                cuts = _k_cuts(t.part.lo[ax], t.part.hi[ax], kp)
                 if c >= len(cuts):
                     continue
                 sub = _with_range(t.part, ax, *cuts[c])
@@ -938,12 +948,22 @@ class _Executor:
             m, box = native_plan(policy, self._work_loops(w, s, task_loops), leaf, plan.defs)
             out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
                                   plan.out_access.tensor.dims)
-            tiles = {key: DeviceTile(name, rect, self.operand(g, name, rect, hids), self.store[name].dims)
-                     for key, (name, rect, hids) in w.operands.items()}
+            tiles, lazy = {}, []
+            for key, (name, rect, hids) in w.operands.items():
+                h = self.prog.holdings[hids[0]]
+                if len(hids) == 1 and h.rect.contains(rect) and name in split["axis"]:
+                    # a view; input slabs still uploading are waited for piece by piece below
+                    buf = _slice(self.holding_buf(hids[0]), h.rect, rect)
+                    lazy.append((hids[0], rect, split["axis"][name]))
+                else:
+                    buf = self.operand(g, name, rect, hids)
+                tiles[key] = DeviceTile(name, rect, buf, self.store[name].dims)
             ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
-            for c, (a, b) in enumerate(_k_cuts(*box[kv])):
+            for c, (a, b) in enumerate(_k_cuts(*box[kv], self.store.first_step_pieces)):
                 if c:
                     st.wait_event(events[g][min(c, len(events[g]) - 1)])
+                for hid, rect, ax in lazy:
+                    self.wait_piece(st, hid, _with_range(rect, ax, a, b))
                 sub = dict(box)
                 sub[kv] = (a, b)
                 run_native_box(m, leaf, sub, out_tile, ins, st, acc if c == 0 else 1)
