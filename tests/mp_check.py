@@ -91,6 +91,29 @@ def main():
                 failures.append(f"split+peer {b.machine} rep {rep}")
     rt.SPLIT_MIN_BYTES = saved
 
+    # e2e shape: inputs uploading in k-slabs from host pieces, pipelined first step in 8 slab-aligned
+    # pieces, row-streamed output (bench.py bench_gemm_e2e), checked against the oracle
+    from oracle.generator import generate_box
+    rt.SPLIT_MIN_BYTES = 0
+    b = td.cannon(2, 2, dims=(520, 392, 1024)) if size >= 4 else td.summa(2, 1, dims=(600, 160, 1024), chunk=512)
+    cin = b.scheduled()
+    st2 = td.RegionStore(b.machine, world)
+    for k, name in enumerate(b.input_names):
+        dist = b.distributions[name]
+        pieces = {c: generate_box(dist.tensor_dims, box.lo, box.shape, 12, k + 1, 0) for c, box in st2.local_colors(dist)}
+        st2.place_local(name, dist, pieces, defer=True)
+        for c, _ in st2.local_colors(dist):
+            st2.upload(name, c, slabs=8 if name == "A" else 4, axis=1 if name == "A" else 0, copy_stream=k)
+    out = b.statement.lhs.tensor.name
+    st2.place_zeros(out, b.distributions[out])
+    st2.stream_rows, st2.first_step_pieces = 4, 8
+    td.execute(cin, st2)
+    ins = {n: generate(b.statement.tensors()[n].dims, 12, k + 1, 0) for k, n in enumerate(b.input_names)}
+    want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+    if not np.array_equal(st2[out].tensor.data, want):
+        failures.append(f"e2e-shape {b.name} {b.machine}")
+    rt.SPLIT_MIN_BYTES = saved
+
     # output streaming: the last step's leaves in row pieces with per-piece events (e2e D2H overlap)
     for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.summa(2, 1, dims=(600, 160, 512), chunk=128)):
         cin, store = b.prepare(seed=8, mode=0, world=world)
