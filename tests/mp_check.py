@@ -99,10 +99,10 @@ def main():
     cin = b.scheduled()
     st2 = td.RegionStore(b.machine, world)
     for k, name in enumerate(b.input_names):
-        dist = b.distributions[name]
-        pieces = {c: generate_box(dist.tensor_dims, box.lo, box.shape, 12, k + 1, 0) for c, box in st2.local_colors(dist)}
-        st2.place_local(name, dist, pieces, defer=True)
-        for c, _ in st2.local_colors(dist):
+        dd = b.distributions[name]
+        pieces = {c: generate_box(dd.tensor_dims, box.lo, box.shape, 12, k + 1, 0) for c, box in st2.local_colors(dd)}
+        st2.place_local(name, dd, pieces, defer=True)
+        for c, _ in st2.local_colors(dd):
             st2.upload(name, c, slabs=8 if name == "A" else 4, axis=1 if name == "A" else 0, copy_stream=k)
     out = b.statement.lhs.tensor.name
     st2.place_zeros(out, b.distributions[out])
