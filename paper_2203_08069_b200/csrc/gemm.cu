@@ -383,7 +383,11 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(44, 64, 128, 16, 32, 64, 3, 0)             \
   X(47, 64, 64, 16, 32, 32, 3, 4)              \
   X(48, 128, 32, 16, 32, 32, 3, 4)             \
-  X(50, 128, 64, 16, 64, 32, 4, 0)
+  X(50, 128, 64, 16, 64, 32, 4, 0)              \
+  X(51, 128, 32, 16, 32, 16, 3, 3)              \
+  X(52, 64, 32, 16, 32, 16, 3, 6)               \
+  X(53, 128, 32, 16, 64, 16, 3, 3)              \
+  X(54, 64, 32, 16, 16, 32, 3, 6)
 
 // Tile history on B200 (scratch/tune2.py, tune_n32.py, tune_n64.py; 16384^3
 // unless noted):
