@@ -186,7 +186,19 @@ class InboxSet:
                 ptr = C.c_void_p()
                 nbytes = 8 * max(1, math.prod(ib.shape))
                 h = C.create_string_buffer(IPC_HANDLE_BYTES) if multi and ib.writer_dev is None else None
-                _native.call("td_peer_alloc", ib.home_dev.index, nbytes, C.byref(ptr), h)
+                try:
+                    _native.call("td_peer_alloc", ib.home_dev.index, nbytes, C.byref(ptr), h)
+                except Exception:
+                    # PyTorch's cache may hold the free memory: release it once, then
+                    # fall back to the NCCL write-back if there is still no room
+                    import torch
+                    with torch.cuda.device(ib.home_dev):
+                        torch.cuda.empty_cache()
+                    try:
+                        _native.call("td_peer_alloc", ib.home_dev.index, nbytes, C.byref(ptr), h)
+                    except Exception:
+                        ok = False
+                        break
                 ib.home_ptr = ptr.value
                 if ib.writer_dev is not None:
                     ib.writer_ptr = ib.home_ptr
