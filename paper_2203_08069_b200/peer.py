@@ -253,6 +253,16 @@ class InboxSet:
 MAX_SETS = 2
 
 
+class _Empty:
+    inboxes: dict = {}
+
+    def by_task(self) -> dict:
+        return {}
+
+
+_NO_INBOXES = _Empty()
+
+
 def inbox_set(prog, world, gpu_of) -> InboxSet:
     """The InboxSet of (prog, world), created on first use.  Creation is
     collective in SPMD jobs (handle exchange): every rank reaches it at the
@@ -262,6 +272,8 @@ def inbox_set(prog, world, gpu_of) -> InboxSet:
     hit = reg.get(id(prog))
     if hit is not None and hit.prog is prog:
         return hit
+    if not eligible_commits(prog, gpu_of):     # nothing to map: do not evict a useful set
+        return _NO_INBOXES
     while len(reg) >= MAX_SETS:
         old = reg.pop(next(iter(reg)))
         old.release(world)
