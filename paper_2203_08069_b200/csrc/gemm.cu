@@ -383,11 +383,7 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(44, 64, 128, 16, 32, 64, 3, 0)             \
   X(47, 64, 64, 16, 32, 32, 3, 4)              \
   X(48, 128, 32, 16, 32, 32, 3, 4)             \
-  X(50, 128, 64, 16, 64, 32, 4, 0)              \
-  X(51, 128, 32, 16, 32, 16, 3, 3)              \
-  X(52, 64, 32, 16, 32, 16, 3, 6)               \
-  X(53, 128, 32, 16, 64, 16, 3, 3)              \
-  X(54, 64, 32, 16, 16, 32, 3, 6)
+  X(50, 128, 64, 16, 64, 32, 4, 0)
 
 // Tile history on B200 (scratch/tune2.py, tune_n32.py, tune_n64.py; 16384^3
 // unless noted):
@@ -398,7 +394,11 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // TTM shape (M = 2^20, N = 64, K = 1024): config 20 35.0, config 47 36.0.
 // N <= 32 (MTTKRP / TTM with a rank-32 factor; the A panel streams from HBM
 // at ~4.4 TB/s): LDGSTS 128x32x8 4 stages (config 34) 33.6, TMA 128x32x16
-// 3 stages (config 48) 35.2.
+// 3 stages (config 48) 35.2.  Also measured at N = 32 (round 1, no gain):
+// TMA 128x32 with BK 12 / 3 stages 34.8, BK 16 / 2 stages / 4 CTAs 35.3,
+// BK 8 / 5 stages 34.7, 64x32 / 6 CTAs 34.9, 256x32 33.7, 8 warps of 32x16
+// 34.3, 64x32 with 16x32 warps 35.1; and the MTTKRP tail wave split into
+// half-k CTAs 34.8-35.1 (CTA waves are not synchronous).
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;

@@ -360,10 +360,6 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
     case 13: return launch_mttkrp_gemm(st, a, 35);
     case 15: return launch_mttkrp_gemm(st, a, 43);
     case 18: return launch_mttkrp_gemm(st, a, 48);
-    case 19: return launch_mttkrp_gemm(st, a, 51);
-    case 20: return launch_mttkrp_gemm(st, a, 52);
-    case 21: return launch_mttkrp_gemm(st, a, 53);
-    case 22: return launch_mttkrp_gemm(st, a, 54);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;
