@@ -447,7 +447,7 @@ def bench_kernels(job, steps, warmup):
     results["summa_1024_2x2"] = {"config": "summa 2x2 dims (1024, 1024, 1024) chunk 128", "value":
                                  2.0 * 1024 ** 3 * 20 / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
                                  "ms_per_step": ms / 20, "scaling": "strong (fixed size)"}
-    if job.world.ngpus == 1:   # the same launch captured once as a CUDA graph and replayed
+    if job.world.ngpus == 1 or job.world.nprocs == job.world.ngpus:   # captured once as a CUDA graph, replayed
         from paper_2203_08069_b200.runtime import CapturedLaunch
         cap = CapturedLaunch(cin, store)
         gms = job.timed(cap.replay, 50, 5)

@@ -561,7 +561,7 @@ class _Executor:
                     continue
                 ib = self.inbox.get(t.coord)
                 if ib is not None:
-                    if ib.credit is not None:       # the home has released the inbox
+                    if ib.credit is not None and not _CAPTURING:   # the home has released the inbox
                         self.cstream(g).wait_event(ib.credit)
                     self.out_bufs[t.coord] = ib.writer_view()
                     continue
@@ -1104,7 +1104,7 @@ class _Executor:
                     recvs.append((ib.writer_gpu, ib.home_gpu, tw))
             self._nccl(sends, recvs)
             for ib, tw, th in tokens:
-                if tw is not None:
+                if tw is not None and not _CAPTURING:
                     ev = self.torch.cuda.Event()
                     ev.record(self.xstream(ib.writer_gpu))
                     ib.credit = ev
@@ -1181,21 +1181,31 @@ def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: 
     return trace
 
 
+_CAPTURING = False      # inside CapturedLaunch's capture: no cross-launch events
+
+
 class CapturedLaunch:
     """One `execute` of a scheduled statement on a store, captured once into a
-    CUDA graph and replayed: every leaf, copy, event fork/join and
-    stream-ordered allocation of the launch becomes one `graph.replay()`,
-    removing the host issue cost that dominates small launches (SUMMA 1024^3
-    on 2x2: 8 steps x 4 tasks).  Inputs are read in place, so refresh them
+    CUDA graph and replayed: every leaf, copy, NCCL send / receive /
+    broadcast, event fork/join and stream-ordered allocation of the launch
+    becomes one `graph.replay()`, removing the host issue cost that dominates
+    small launches (SUMMA 1024^3 on 2x2: 8 steps x 4 tasks) -- the step loop
+    no longer runs in Python.  Inputs are read in place, so refresh them
     between replays by writing into their pieces; with ``reset_output`` the
     output pieces are zeroed inside the graph (a fresh run_statement
-    output).  Single-process, GPU-local programs only (NCCL capture across
-    processes is not attempted)."""
+    output).  Jobs on one GPU, or SPMD jobs with one GPU per process
+    (`configure_distributed`): every rank captures its own GPU's part of the
+    same program, so the captured NCCL calls pair up at every replay; replays
+    must then be issued by every rank, like `execute`.  Replays on one stream
+    are ordered, so the peer-inbox credit (`peer.py`) needs no event across
+    replays."""
 
     def __init__(self, stmt, store: RegionStore, *, leaf_policy: str = "auto", reset_output: bool = True):
+        global _CAPTURING
         torch = torch_mod()
-        if store.world.nprocs > 1 or store.world.ngpus > 1:
-            raise ConfigError("CapturedLaunch supports single-GPU jobs")
+        W = store.world
+        if W.ngpus > 1 and not (W.nprocs == W.ngpus and len(W.owned) == 1):
+            raise ConfigError("CapturedLaunch supports one-GPU jobs and SPMD jobs with one GPU per process")
         self.stmt, self.store = stmt, store
         plan_trace = ExecutionTrace(store.machine)
         prog = _plan_cached(stmt, store, plan_trace, False)
@@ -1206,12 +1216,16 @@ class CapturedLaunch:
         execute(stmt, store, record_requirements=False, leaf_policy=leaf_policy)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
-            if reset_output:
-                for buf in store[self.out].pieces.values():
-                    buf.zero_()
-            store[self.out].zeroed = reset_output
-            execute(stmt, store, record_requirements=False, leaf_policy=leaf_policy)
+        _CAPTURING = True
+        try:
+            with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+                if reset_output:
+                    for buf in store[self.out].pieces.values():
+                        buf.zero_()
+                store[self.out].zeroed = reset_output
+                execute(stmt, store, record_requirements=False, leaf_policy=leaf_policy)
+        finally:
+            _CAPTURING = False
         self.trace = plan_trace
 
     def replay(self) -> None:
