@@ -114,28 +114,6 @@ def main():
         failures.append(f"e2e-shape {b.name} {b.machine}")
     rt.SPLIT_MIN_BYTES = saved
 
-    # multi-GPU CUDA graphs: one execute (NCCL groups, peer-inbox tokens, leaves) captured per rank and replayed
-    from paper_2203_08069_b200.runtime import CapturedLaunch
-    gcases = [td.summa(2, 1, dims=(200, 160, 512), chunk=64), td.cosma_like((1, 1, 2), (1, 1, 1), dims=(136, 120, 300))]
-    if size >= 4:
-        gcases += [td.cannon(2, 2, dims=(200, 144, 176)), td.mttkrp(2, 2, dims=(40, 32, 48, 36)),
-                   td.summa(2, 2, dims=(256, 256, 256), chunk=32)]
-    for b in gcases:
-        cin, store = b.prepare(seed=14, mode=0, world=world)
-        out = b.statement.lhs.tensor.name
-        cap = CapturedLaunch(cin, store)
-        ins = {n: generate(b.statement.tensors()[n].dims, 14, k + 1, 0) for k, n in enumerate(b.input_names)}
-        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
-        for rep in range(3):
-            cap.replay()
-            if not np.array_equal(store[out].tensor.data, want):
-                failures.append(f"graph {b.name} {b.machine} replay {rep}")
-        td.execute(cin, store)    # eager again after replays (accumulates onto the last replay's output)
-        store.zero(out)
-        td.execute(cin, store)
-        if not np.array_equal(store[out].tensor.data, want):
-            failures.append(f"graph {b.name} {b.machine} eager after replays")
-
     # output streaming: the last step's leaves in row pieces with per-piece events (e2e D2H overlap)
     for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.summa(2, 1, dims=(600, 160, 512), chunk=128)):
         cin, store = b.prepare(seed=8, mode=0, world=world)
@@ -195,6 +173,34 @@ def main():
     td.redistribute(store, "T", new, trace)
     if not np.array_equal(store["T"].tensor.data, data.data):
         failures.append("redistribute")
+
+    # multi-GPU CUDA graphs: one execute (NCCL groups, peer-inbox tokens, leaves) captured per rank and
+    # replayed.  Last: after a capture NCCL synchronises eager work on the communicator with the graph's;
+    # the graphs are destroyed before the communicators are
+    from paper_2203_08069_b200.runtime import CapturedLaunch
+    gcases = [td.summa(2, 1, dims=(200, 160, 512), chunk=64), td.cosma_like((1, 1, 2), (1, 1, 1), dims=(136, 120, 300))]
+    if size >= 4:
+        gcases += [td.cannon(2, 2, dims=(200, 144, 176)), td.mttkrp(2, 2, dims=(40, 32, 48, 36)),
+                   td.summa(2, 2, dims=(256, 256, 256), chunk=32)]
+    for b in gcases:
+        cin, store = b.prepare(seed=14, mode=0, world=world)
+        out = b.statement.lhs.tensor.name
+        cap = CapturedLaunch(cin, store)
+        ins = {n: generate(b.statement.tensors()[n].dims, 14, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+        for rep in range(3):
+            cap.replay()
+            if not np.array_equal(store[out].tensor.data, want):
+                failures.append(f"graph {b.name} {b.machine} replay {rep}")
+        td.execute(cin, store)    # eager again after replays (accumulates onto the last replay's output)
+        store.zero(out)
+        td.execute(cin, store)
+        if not np.array_equal(store[out].tensor.data, want):
+            failures.append(f"graph {b.name} {b.machine} eager after replays")
+        del cap
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
 
     flag = torch.tensor([len(failures)], device="cuda")
     dist.all_reduce(flag)
