@@ -398,7 +398,8 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // TMA 128x32 with BK 12 / 3 stages 34.8, BK 16 / 2 stages / 4 CTAs 35.3,
 // BK 8 / 5 stages 34.7, 64x32 / 6 CTAs 34.9, 256x32 33.7, 8 warps of 32x16
 // 34.3, 64x32 with 16x32 warps 35.1; and the MTTKRP tail wave split into
-// half-k CTAs 34.8-35.1 (CTA waves are not synchronous).
+// half-k CTAs 34.8-35.1 (CTA waves are not synchronous); a persistent
+// row-sum kernel keeping the TMA ring running across tiles 31.0-31.7.
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;
@@ -456,7 +457,6 @@ int dgemm_dispatch(cudaStream_t st, int64_t batch, GemmArgs a, int config = -1) 
   X(35, 128, 32, 16, 32, 32, 4)
 
 int dgemm_rowsum_tile_rows(int config) {
-  if (config >= 100) config -= 100;   // persistent variant of a TMA config
   switch (config) {
 #define TD_ROWSUM_BM(id, BM, BN, BK, WM, WN, ST) \
   case id:                                        \
@@ -471,25 +471,7 @@ int dgemm_rowsum_tile_rows(int config) {
   }
 }
 
-// persistent TMA row-sum kernels (ids 100 + TMA config)
-static int rowsum_persistent(cudaStream_t st, int config, int64_t batch, const GemmArgs& a) {
-  switch (config) {
-#define TD_ROWSUM_PERSIST_CASE(id, BM, BN, BK, WM, WN, ST, MINB) \
-  case 100 + id:                                                 \
-    return launch_rowsum_persistent<BM, BN, BK, WM, WN, ST, MINB>(st, batch, a);
-    TD_GEMM_TMA_CONFIGS(TD_ROWSUM_PERSIST_CASE)
-#undef TD_ROWSUM_PERSIST_CASE
-    default:
-      set_error("mttkrp: unknown persistent row-sum config %d", config);
-      return TD_ERR_ARG;
-  }
-}
-
 int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
-  if (config >= 100) {
-    if (tma_ok(batch, a)) return rowsum_persistent(st, config, batch, a);
-    config -= 100;   // operands the copy engine cannot address: the per-tile kernels below
-  }
   const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                     (batch == 1 || a.sA % 2 == 0);
   for (int64_t done = 0; done < batch;) {  // grid.y is limited to 65535

@@ -209,152 +209,6 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
-// Persistent variant for the MTTKRP row-sum GEMM (EPI = 1): one CTA per resident
-// slot walks tiles t = blockIdx.x, + gridDim.x, ... and the TMA ring runs
-// across tile boundaries (k-iteration counter g over all of the CTA's tiles),
-// so the next tile's first stages load while this tile's epilogue runs and no
-// CTA pays a pipeline fill per tile.  Same fragment layouts and epilogue order
-// as dgemm_tma_kernel (bitwise the same row sums).
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
-__global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
-                                  TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
-dgemm_tma_rowsum_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            GemmArgs p, int batch) {
-  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
-  extern __shared__ __align__(128) unsigned char tma_smem_raw[];
-  __shared__ __align__(8) uint64_t full[STAGES];
-  __shared__ double red[Cfg::WARPS_M * BN];
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 127) & ~uintptr_t(127));
-  double* As = smem;
-  double* Bs = smem + STAGES * Cfg::A_STAGE;
-
-  const int64_t M = p.M, N = p.N, K = p.K;
-  const int per_batch = p.tiles_m * p.tiles_n;
-  const int64_t total = int64_t(per_batch) * batch;
-  const int64_t my_tiles = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int ktiles = (int)ceil_div(K, BK);
-  const int64_t my_iters = my_tiles * ktiles;
-
-  // tile j of this CTA -> (batch, M-tile, N-tile), grouped rasterisation inside a batch
-  auto coords = [&](int64_t j, int& bz, int& tm, int& tn) {
-    const int64_t t = blockIdx.x + j * gridDim.x;
-    bz = (int)(t / per_batch);
-    const int tile = (int)(t - int64_t(bz) * per_batch);
-    const int pg = p.group * p.tiles_n;
-    const int first_m = (tile / pg) * p.group;
-    const int gsize = min(p.tiles_m - first_m, p.group);
-    const int in_g = tile % pg;
-    tm = first_m + in_g % gsize;
-    tn = in_g / gsize;
-  };
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  const int wm0 = (warp / Cfg::WARPS_N) * WM;
-  const int wn0 = (warp % Cfg::WARPS_N) * WN;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  auto issue = [&](int64_t g) {  // g-th k-iteration of this CTA (tile g / ktiles)
-    const int s = (int)(g % STAGES);
-    const int64_t j = g / ktiles;
-    const int kt = (int)(g - j * ktiles);
-    int bz, tm, tn;
-    coords(j, bz, tm, tn);
-    mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-    tma_load_4d(As + s * Cfg::A_STAGE, &tmA, 0, tm * BM, kt * (BK / 4), bz, &full[s]);
-    tma_load_4d(Bs + s * Cfg::B_STAGE, &tmB, 0, kt * BK, (tn * BN) / 4, p.sB ? bz : 0, &full[s]);
-  };
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s)
-      if (s < my_iters) issue(s);
-  }
-
-  const int a_off = (wm0 + (lane >> 2)) * 4 + (lane & 3);
-  const int b_off = ((wn0 + (lane >> 2)) / 4) * BK * 4 + (lane & 3) * 4 + ((lane >> 2) & 3);
-
-  int64_t g = 0;
-  for (int64_t j = 0; j < my_tiles; ++j) {
-    double acc[Cfg::FM][Cfg::FN][2];
-#pragma unroll
-    for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-      for (int q = 0; q < Cfg::FN; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
-
-    for (int kt = 0; kt < ktiles; ++kt, ++g) {
-      mbar_wait(&full[g % STAGES], (uint32_t)((g / STAGES) & 1));
-      __syncthreads();  // every warp is done with the stage the next copy overwrites
-      if (tid == 0 && g + STAGES - 1 < my_iters) issue(g + STAGES - 1);
-      const double* as = As + (g % STAGES) * Cfg::A_STAGE + a_off;
-      const double* bs = Bs + (g % STAGES) * Cfg::B_STAGE + b_off;
-#pragma unroll
-      for (int kq = 0; kq < BK / 4; ++kq) {
-        double af[Cfg::FM], bf[Cfg::FN];
-#pragma unroll
-        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[kq * BM * 4 + i * 32];
-#pragma unroll
-        for (int q = 0; q < Cfg::FN; ++q) bf[q] = bs[kq * 16 + q * 2 * BK * 4];
-#pragma unroll
-        for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-          for (int q = 0; q < Cfg::FN; ++q) dmma_8x8x4(acc[i][q][0], acc[i][q][1], af[i], bf[q]);
-      }
-    }
-
-    // row-sum epilogue of tile j (as dgemm_tma_kernel, EPI = 1), into its own smem
-    int bz, tm, tn;
-    coords(j, bz, tm, tn);
-    const int m0 = tm * BM, n0 = tn * BN;
-    double part[Cfg::FN][2];
-#pragma unroll
-    for (int q = 0; q < Cfg::FN; ++q) part[q][0] = part[q][1] = 0.0;
-#pragma unroll
-    for (int i = 0; i < Cfg::FM; ++i) {
-      const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
-      const double* hrow = p.H + r * p.ldh;
-#pragma unroll
-      for (int q = 0; q < Cfg::FN; ++q) {
-        const int64_t c = n0 + wn0 + q * 8 + (lane & 3) * 2;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (r < M && c + h < N) part[q][h] += hrow[c + h] * acc[i][q][h];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < Cfg::FN; ++q)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double v = part[q][h];
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        part[q][h] = v;
-      }
-    __syncthreads();  // the previous tile's readers of red are done
-    if (lane < 4) {
-#pragma unroll
-      for (int q = 0; q < Cfg::FN; ++q)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) red[(warp / Cfg::WARPS_N) * BN + wn0 + q * 8 + lane * 2 + h] = part[q][h];
-    }
-    __syncthreads();
-    double* C = p.C + int64_t(bz) * p.sC;
-    for (int c = tid; c < BN; c += Cfg::THREADS) {
-      double v = red[c];
-#pragma unroll
-      for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
-      if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
-    }
-  }
-}
-
 // ---- host side: tensor maps through the driver entry point (no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -408,29 +262,6 @@ static int launch_gemm_tma(cudaStream_t st, int64_t batch, GemmArgs a) {
   dim3 grid((unsigned)tiles, (unsigned)batch);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ma, mb, a);
   return check_launch("dgemm_tma_kernel");
-}
-
-// persistent row-sum launch: one CTA per resident slot (occupancy x SMs)
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
-static int launch_rowsum_persistent(cudaStream_t st, int64_t batch, GemmArgs a) {
-  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
-  auto kern = dgemm_tma_rowsum_persistent<BM, BN, BK, WM, WN, STAGES, MINB>;
-  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-  CUtensorMap ma, mb;
-  if (int rc = make_sliced_map(&ma, a.A, a.M, a.K, a.lda, batch, a.sA, BM, BK)) return rc;
-  if (int rc = make_sliced_map(&mb, a.B, a.K, a.N, a.ldb, a.sB ? batch : 1, a.sB, BK, BN)) return rc;
-  a.tiles_m = (int)ceil_div(a.M, BM);
-  a.tiles_n = (int)ceil_div(a.N, BN);
-  a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);
-  int dev = 0, sms = 0, per_sm = 0;
-  TD_CUDA(cudaGetDevice(&dev));
-  TD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  TD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM_BYTES));
-  const int64_t total = int64_t(a.tiles_m) * a.tiles_n * batch;
-  TD_REQUIRE(batch < (1ll << 31) && total < (1ll << 40), "rowsum: grid too large");
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, int64_t(std::max(1, per_sm)) * sms));
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ma, mb, a, (int)batch);
-  return check_launch("dgemm_tma_rowsum_persistent");
 }
 
 }  // namespace td

@@ -360,9 +360,6 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
     case 13: return launch_mttkrp_gemm(st, a, 35);
     case 15: return launch_mttkrp_gemm(st, a, 43);
     case 18: return launch_mttkrp_gemm(st, a, 48);
-    case 19: return launch_mttkrp_gemm(st, a, 148);   // persistent 128x32x16 (config 48 tiles)
-    case 20: return launch_mttkrp_gemm(st, a, 147);   // persistent 64x64x16
-    case 21: return launch_mttkrp_gemm(st, a, 143);   // persistent 128x32x16, no min-blocks bound
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;
