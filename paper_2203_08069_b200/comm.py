@@ -112,7 +112,7 @@ class World:
 
     def close(self):
         for s in self.inbox_sets.values():
-            s.free()
+            s.release(self)        # after a device sync: no leaf still writes an inbox
         self.inbox_sets = {}
         for grp in self._groups.values():
             for h in grp.values():
