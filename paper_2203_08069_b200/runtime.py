@@ -945,6 +945,11 @@ class _Executor:
             st = self.cstream(g)
             st.wait_event(events[g][0])
             acc = 0 if w.task.coord in self.inbox else 1
+            if any(rect is None for _, rect, _ in w.operands.values()):
+                if not acc:   # an empty access: the partial is all zeros
+                    _native.call("td_fill", stream_handle(st), C.c_void_p(self.out_bufs[w.task.coord].data_ptr()),
+                                 self.out_bufs[w.task.coord].numel(), 0.0)
+                continue
             m, box = native_plan(policy, self._work_loops(w, s, task_loops), leaf, plan.defs)
             out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
                                   plan.out_access.tensor.dims)
