@@ -392,9 +392,11 @@ def bench_gemm_e2e(job, bundle, cin, steps):
     return {"value": flop * steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(job.sum_over_ranks(h2d)),
             "d2h_bytes_per_step": int(job.sum_over_ranks(d2h)), "ms_per_step": dt * 1e3 / steps,
             "steps": steps, "algorithm": f"{bundle.name} {bundle.machine}", "rows_exact": ok,
-            "how": "pinned host pieces -> RegionStore.place_local (async H2D in k-slabs on two copy streams, "
-                   "overlapped with the leaves of earlier k-chunks) -> execute -> D2H of each home output "
-                   "piece as soon as it is final (store.done events); host wall clock, max over ranks"}
+            "how": "pinned host pieces -> RegionStore.place_local (async H2D in k-slabs on two copy streams; "
+                   "leaves and NCCL sends wait only for the slabs they touch: p=1 task-major k-chunks, p>1 "
+                   "the pipelined first step in the A upload's 8 k-slabs) -> execute -> D2H of output rows as "
+                   "soon as their row piece of the last step is done (RegionStore.stream_rows / row_done); "
+                   "host wall clock, max over ranks"}
 
 
 # ------------------------------------------------------------------ other configs
