@@ -323,10 +323,17 @@ def bench_gemm_e2e(job, bundle, cin, steps):
             s2.place_local(name, bundle.distributions[name], host[name], defer=True)
         if bundle.machine.flat_dims == (4, 1) and job.world.ngpus == 1:
             # task-major on one GPU: task 0 needs A0 and every B k-slab first,
-            # in k order; the other A row blocks can follow
-            for s in range(8):
-                s2.upload("B", (s // 2, 0), slabs=2, axis=0, only=[s % 2])
-                s2.upload("A", (0, 0), slabs=8, axis=1, only=[s])
+            # in k order; the other A row blocks can follow.  The first k-chunk
+            # arrives in 8 sub-slabs that task 0's first GEMM consumes piece by
+            # piece (first_step_pieces), so compute starts after 1/64 of A0 and B
+            for q in range(8):
+                s2.upload("B", (0, 0), slabs=16, axis=0, only=[q])
+                s2.upload("A", (0, 0), slabs=64, axis=1, only=[q])
+            s2.upload("B", (0, 0), slabs=16, axis=0, only=range(8, 16))
+            for s in range(1, 8):
+                if s >= 2:
+                    s2.upload("B", (s // 2, 0), slabs=2, axis=0, only=[s % 2])
+                s2.upload("A", (0, 0), slabs=64, axis=1, only=range(8 * s, 8 * s + 8))
             for q in range(1, 4):
                 s2.upload("A", (q, 0), slabs=8, axis=1)
         else:
@@ -338,8 +345,9 @@ def bench_gemm_e2e(job, bundle, cin, steps):
         # rows download as soon as they are done (at p > 1 every output piece is final
         # only after the last step; at p = 1 this shortens the last row block's tail)
         s2.stream_rows = 4
-        # p > 1: the pipelined first step moves and multiplies k in the A upload's 8 slabs
-        s2.first_step_pieces = nslabs["A"]
+        # the first step's GEMM runs in 8 k-pieces that wait only for their own slabs (p > 1:
+        # the pipelined first step, in the A upload's 8 slabs; p = 1: task 0's first k-chunk)
+        s2.first_step_pieces = 8
         td.execute(cin, s2, record_requirements=False)
         nbytes = 0
         for color, box, _ in out_dist.pieces():

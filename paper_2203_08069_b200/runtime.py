@@ -936,7 +936,6 @@ class _Executor:
         plan = self.plan
         task_loops, leaf = _loops_of(plan.task_body)
         policy, _ = _leaf_choice(plan.relations, [v for v, _, _ in task_loops], self.policy)
-        rhs = accesses_of(leaf.rhs)
         kv = split["kv"]
         for w in works:
             g = self.gpu(w.task.coord)
@@ -950,30 +949,41 @@ class _Executor:
                     _native.call("td_fill", stream_handle(st), C.c_void_p(self.out_bufs[w.task.coord].data_ptr()),
                                  self.out_bufs[w.task.coord].numel(), 0.0)
                 continue
-            m, box = native_plan(policy, self._work_loops(w, s, task_loops), leaf, plan.defs)
-            out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
-                                  plan.out_access.tensor.dims)
-            tiles, lazy = {}, []
-            for key, (name, rect, hids) in w.operands.items():
-                h = self.prog.holdings[hids[0]]
-                if len(hids) == 1 and h.rect.contains(rect) and name in split["axis"]:
-                    # a view; input slabs still uploading are waited for piece by piece below
-                    buf = _slice(self.holding_buf(hids[0]), h.rect, rect)
-                    lazy.append((hids[0], rect, split["axis"][name]))
-                else:
-                    buf = self.operand(g, name, rect, hids)
-                tiles[key] = DeviceTile(name, rect, buf, self.store[name].dims)
-            ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
-            for c, (a, b) in enumerate(_k_cuts(*box[kv], self.store.first_step_pieces)):
-                if c:
-                    st.wait_event(events[g][min(c, len(events[g]) - 1)])
-                for hid, rect, ax in lazy:
-                    self.wait_piece(st, hid, _with_range(rect, ax, a, b))
-                sub = dict(box)
-                sub[kv] = (a, b)
-                run_native_box(m, leaf, sub, out_tile, ins, st, acc if c == 0 else 1)
-            for e in events[g][1:]:
-                st.wait_event(e)
+            self._run_k_pieces(w, s, g, st, acc, self._work_loops(w, s, task_loops), leaf, policy, kv,
+                               events[g])
+
+    def _run_k_pieces(self, w, s, g, st, acc, loops, leaf, policy, kv, events=None) -> None:
+        """One native GEMM leaf in the k-pieces of `_k_cuts` (first_step_pieces):
+        operand views are taken without waiting, and piece c waits only for the
+        input slabs it touches (progressive placement) and, when `events` is
+        given, for the transfers of pieces <= c."""
+        plan = self.plan
+        rhs = accesses_of(leaf.rhs)
+        m, box = native_plan(policy, loops, leaf, plan.defs)
+        out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
+                              plan.out_access.tensor.dims)
+        kaxis = {a.tensor.name: a.var_names.index(kv) for a in rhs if kv in a.var_names}
+        tiles, lazy = {}, []
+        for key, (name, rect, hids) in w.operands.items():
+            h = self.prog.holdings[hids[0]]
+            if len(hids) == 1 and h.rect.contains(rect) and name in kaxis:
+                # a view; input slabs still uploading are waited for piece by piece below
+                buf = _slice(self.holding_buf(hids[0]), h.rect, rect)
+                lazy.append((hids[0], rect, kaxis[name]))
+            else:
+                buf = self.operand(g, name, rect, hids)
+            tiles[key] = DeviceTile(name, rect, buf, self.store[name].dims)
+        ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
+        for c, (a, b) in enumerate(_k_cuts(*box[kv], self.store.first_step_pieces)):
+            if c and events:
+                st.wait_event(events[min(c, len(events) - 1)])
+            for hid, rect, ax in lazy:
+                self.wait_piece(st, hid, _with_range(rect, ax, a, b))
+            sub = dict(box)
+            sub[kv] = (a, b)
+            run_native_box(m, leaf, sub, out_tile, ins, st, acc if c == 0 else 1)
+        for e in (events or [])[1:]:
+            st.wait_event(e)
 
     def compute(self, works, s):
         plan = self.plan
@@ -997,6 +1007,13 @@ class _Executor:
                 if s >= 0 and plan.step_var is not None and v == plan.step_var.var:
                     lo, hi = s, s + 1
                 loops.append((v, lo, hi))
+            if (not plugins and s == 0 and self.store.first_step_pieces > 2 and self.store.ready
+                    and w.task.coord == self._first_task(g) and self._progressive_gemm(loops, leaf, policy)):
+                # inputs still arriving in k-slabs (e2e): the GPU's first GEMM in k-pieces, each
+                # waiting only for its own slabs
+                self._run_k_pieces(w, s, g, st, acc, loops, leaf, policy,
+                                   contracted_var(native_plan(policy, loops, leaf, plan.defs)[0], leaf))
+                continue
             out_tile = DeviceTile(plan.out_name, w.task.out_rect, self.out_bufs[w.task.coord],
                                   plan.out_access.tensor.dims)
             tiles = {}
@@ -1012,6 +1029,16 @@ class _Executor:
                               {plan.out_name: out_tile}, plugins, st, self.W.device(g))
             else:
                 run_leaf(policy, loops, leaf, plan.defs, out_tile, ins, st, accumulate=acc)
+
+    def _first_task(self, g):
+        for t in self.plan.tasks:
+            if self.gpu(t.coord) == g and t.out_rect is not None:
+                return t.coord
+        return None
+
+    def _progressive_gemm(self, loops, leaf, policy) -> bool:
+        np_ = native_plan(policy, loops, leaf, self.plan.defs)
+        return np_ is not None and contracted_var(np_[0], leaf) is not None
 
     def _stream_rows(self, w, s, g, loops, leaf, policy, out_tile, ins, st) -> bool:
         """Last step of a task that writes its home piece directly (and alone):
