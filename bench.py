@@ -344,7 +344,7 @@ def bench_gemm_e2e(job, bundle, cin, steps):
         # the last step's leaves of each output piece run in row pieces and each piece's
         # rows download as soon as they are done (at p > 1 every output piece is final
         # only after the last step; at p = 1 this shortens the last row block's tail)
-        s2.stream_rows = 4
+        s2.stream_rows = 8
         # the first step's GEMM runs in 8 k-pieces that wait only for their own slabs (p > 1:
         # the pipelined first step, in the A upload's 8 slabs; p = 1: task 0's first k-chunk)
         s2.first_step_pieces = 8
