@@ -78,6 +78,24 @@ def main():
                             {n: t.data for n, t in ins.items()})
             if not np.array_equal(res.output.data, np.asarray(want)):
                 failures.append(f"split {b.name} {b.machine} seed {seed}")
+    # real-valued inputs: the k-pieces reassociate the k sum, so compare with the whole-step run
+    # within the stated bound |got - want| <= 2 gamma_K (|A||B|)_ij, gamma_K = K u / (1 - K u)
+    b = td.cannon(2, 2, dims=(520, 392, 1000))
+    outs = {}
+    for thr in (0, 1 << 62):
+        rt.SPLIT_MIN_BYTES = thr
+        cin, store = b.prepare(seed=15, mode=1, world=world)
+        td.execute(cin, store)
+        outs[thr] = store["C"].tensor.data.copy()
+    rt.SPLIT_MIN_BYTES = 0
+    a_abs = np.abs(generate(b.statement.tensors()["A"].dims, 15, 1, 1))
+    b_abs = np.abs(generate(b.statement.tensors()["B"].dims, 15, 2, 1))
+    kk = b.statement.extents["k"]
+    u = 2.0 ** -53
+    bound = 2 * (kk * u / (1 - kk * u)) * (a_abs @ b_abs)
+    if not np.all(np.abs(outs[0] - outs[1 << 62]) <= bound):
+        failures.append("split real-valued tolerance")
+
     if size >= 4:
         # split first step + peer inboxes together (Johnson 2x2x2 at 8 GPUs does both), twice in a row
         b = td.cosma_like((2, 1, 2), (1, 1, 1), dims=(130, 96, 1200))
