@@ -135,6 +135,14 @@ class Job:
         self.device = self.world.device(self.world.owned[0])
         self.n_gpus = max(n_gpus, self.size)
 
+    def close(self):
+        # same teardown order as tests/mp_check.py: communicators, then the process group
+        if self.dist is not None:
+            self.torch.cuda.synchronize()
+            self.barrier()
+            self.world.close()
+            self.dist.destroy_process_group()
+
     def barrier(self):
         if self.dist is not None:
             self.dist.barrier(device_ids=[self.device.index])
@@ -556,8 +564,12 @@ def main():
     job = Job(args.gpus)
     gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps)
     kernels = bench_kernels(job, max(2, args.steps // 2), max(3, args.warmup)) if args.workload == "all" else None
-    if job.rank != 0:
-        return
+    if job.rank == 0:
+        report(args, job, gemm, kernels)
+    job.close()
+
+
+def report(args, job, gemm, kernels):
     cpu = None
     if job.n_gpus == 1 and not args.no_cpu_baseline:
         # the headline workload itself (16384^3, ~10 s on the box's cores), one timed run
