@@ -13,7 +13,24 @@ SRCS      := $(CSRC)/capi.cu $(CSRC)/gemm.cu $(CSRC)/mttkrp.cu $(CSRC)/stream.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB       := $(PKG)/libdistal_b200.so
 
-all: $(LIB)
+# The reference (pure Python, nothing to compile) is staged into oracle/_ref as
+# the checker and the reference arm's CPU implementation: oracle/_ref/tendist is
+# its package, oracle/_ref/tests its own unit tests.  oracle/_ref is git-ignored
+# (never committed) but travels to the GPU box with the snapshot.  Only done
+# where the reference checkout exists (this container); the GPU box uses the
+# staged copy.
+REF_PKG   ?= /root/reference/pkg
+REF_OUT   := oracle/_ref
+
+all: $(LIB) ref
+
+ref:
+	@if [ -d $(REF_PKG)/src/tendist ]; then \
+	  rm -rf $(REF_OUT) && mkdir -p $(REF_OUT) && \
+	  cp -r $(REF_PKG)/src/tendist $(REF_OUT)/tendist && cp -r $(REF_PKG)/tests $(REF_OUT)/tests && \
+	  chmod -R u+w $(REF_OUT) && find $(REF_OUT) -name __pycache__ -prune -exec rm -rf {} + ; \
+	  echo "staged the reference into $(REF_OUT)"; \
+	else echo "no reference checkout at $(REF_PKG): keeping $(REF_OUT) as is"; fi
 
 build/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/distal_b200.h
 	@mkdir -p build
@@ -25,4 +42,4 @@ $(LIB): $(OBJS)
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean ref
