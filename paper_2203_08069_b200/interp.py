@@ -310,7 +310,48 @@ def execute_chain(loops, leaf, env, defs, read_tiles, out_tiles, plugins, stream
     for point in itertools.product(*(range(lo, hi) for _, lo, hi in outer)):
         penv = dict(env)
         penv.update({v: x for (v, _, _), x in zip(outer, point)})
-        fn(LeafRuntime(list(inner), leaf, penv, defs, read_tiles, out_tiles, device, stream))
+        if getattr(fn, "device", True):
+            fn(LeafRuntime(list(inner), leaf, penv, defs, read_tiles, out_tiles, device, stream))
+        else:
+            _call_host_plugin(fn, list(inner), leaf, penv, defs, read_tiles, out_tiles, stream, device)
+
+
+def _box_index(rect: HyperRect) -> tuple:
+    return tuple(slice(a, b) for a, b in zip(rect.lo, rect.hi))
+
+
+def _call_host_plugin(fn, inner, leaf, env, defs, read_tiles, out_tiles, stream, device):
+    """The reference's plugin contract (`cin.py:359-379, 441-446`) for a
+    plugin registered without ``device=True``: ``read_store`` holds full-size
+    host DenseTensors in GLOBAL coordinates (the boxes this task-step reads,
+    copied out of HBM -- a leaf only reads inside its iteration box) and
+    ``out_store`` one full-size host tensor holding the task's partial so far
+    (zero at the task's start, as the reference's per-task zeroed output),
+    which the plugin updates in place; the output box is then written back
+    to HBM.  ``execute_point`` evaluates one point with the GPU nest kernel
+    against that host state, so a plugin mixing its own arithmetic with
+    interpreter points sees the reference's order of writes."""
+    torch = torch_mod()
+    name = leaf.lhs.tensor.name
+    out_tile = out_tiles[name]
+    out_box = _box_index(out_tile.rect)
+    with torch.cuda.stream(stream):
+        read = {}
+        for tname, tile in read_tiles.items():
+            full = DenseTensor(tile.dims)
+            full.data[_box_index(tile.rect)] = tile.data.cpu().numpy()
+            read[tname] = full
+        host_out = DenseTensor(out_tile.dims)
+        host_out.data[out_box] = out_tile.data.cpu().numpy()
+        ins = [read_tiles[a.tensor.name] for a in accesses_of(leaf.rhs)]
+
+        def point(penv):
+            out_tile.data.copy_(torch.from_numpy(host_out.data[out_box]))
+            run_nest([(v, x, x + 1) for v, x in penv.items()], leaf, defs, out_tile, ins, stream)
+            host_out.data[out_box] = out_tile.data.cpu().numpy()
+
+        fn(LeafRuntime(inner, leaf, env, defs, read, {name: host_out}, device, stream, point))
+        out_tile.data.copy_(torch.from_numpy(host_out.data[out_box]))
 
 
 def interpret_on_device(stmt, store: dict) -> dict:

@@ -1,11 +1,20 @@
-"""The communication ledger: events, launches and memory high-water.
+"""The communication ledger: events, launches, memory high-water, timings.
 
-`CommEvent` / `ExecutionTrace` keep the reference's record types and
-statistics (reference `pkg/src/tendist/simulator.py:113-269`).  On the
-B200 path every compute-phase `CommEvent` is a real transfer: `runtime.py`
-issues one NCCL send/recv (or a zero-copy same-GPU alias) per event, so the
-ledger is a faithful description of the bytes that crossed NVLink, and the
-reference's traffic anchors double as tests of the collective lowering.
+`CommEvent` and the `ExecutionTrace` query/stats surface keep the
+reference's record types and its stats JSON schema (reference
+`pkg/src/tendist/simulator.py:113-269`) -- the schema is the contract the
+reference's anchor tests and tools read.  The implementation is a small
+group-by engine: every aggregate in the stats (totals, phases, per edge, per
+step, per machine level) is `_rollup(events, key)` over one event filter,
+and `stats()` is assembled from the `_SECTIONS` table.
+
+On the B200 path every compute-phase `CommEvent` is a real transfer:
+`runtime.py` issues one NCCL send/recv (or a zero-copy same-GPU alias) per
+event, so the ledger describes the bytes that crossed NVLink.  When a run
+is timed (`execute(..., timed=True)`), `timings` holds one record per
+launch measured with CUDA events on the executing streams, and `stats()`
+adds a ``"measured"`` section (device milliseconds, GFLOP/s or GB/s, and
+the fraction of the B200 roof) beside the reference's keys.
 """
 
 from __future__ import annotations
@@ -16,8 +25,10 @@ from dataclasses import dataclass, field
 from .distribution import HyperRect
 from .machine import Machine
 
+_record = dataclass(frozen=True)
 
-@dataclass(frozen=True)
+
+@_record
 class CommEvent:
     """One aggregate transfer: ``src`` sends box ``rect`` of ``tensor`` to ``dst``."""
 
@@ -31,7 +42,7 @@ class CommEvent:
     phase: str   # "compute" | "placement"
 
 
-@dataclass(frozen=True)
+@_record
 class TaskInfo:
     coord: tuple
     rank: int
@@ -39,7 +50,7 @@ class TaskInfo:
     out_rect: object = None
 
 
-@dataclass(frozen=True)
+@_record
 class Requirement:
     """What one task needed for one step before sourcing (debug record)."""
 
@@ -50,8 +61,22 @@ class Requirement:
     scope: str   # "launch" | "step"
 
 
-def _tally(events) -> dict:
-    return {"messages": len(events), "elements": sum(e.elements for e in events)}
+def _rollup(events, key=None) -> dict:
+    """{key(e): [messages, elements]} in first-seen order (key None: one bucket)."""
+    acc: dict = {}
+    for e in events:
+        slot = acc.setdefault(None if key is None else key(e), [0, 0])
+        slot[0] += 1
+        slot[1] += e.elements
+    return acc
+
+
+def _pair(counts) -> dict:
+    messages, elements = counts or (0, 0)
+    return {"messages": messages, "elements": elements}
+
+
+_FILTER_FIELDS = {"kind": "kind", "phase": "phase", "tensor": "tensor", "step": "timestep"}
 
 
 class ExecutionTrace:
@@ -63,21 +88,29 @@ class ExecutionTrace:
         self.launches: list = []
         self.requirements: list = []
         self.num_steps = 0
-        self.memory = {p: 0 for p in machine.enumerate()}
-        self.timings: list = []   # B200 addition: per-launch device timings (ms)
+        self.memory = dict.fromkeys(machine.enumerate(), 0)
+        self.timings: list = []
 
+    # -- recording ----------------------------------------------------------
     def bump_memory(self, coord, elements: int) -> None:
-        if elements > self.memory[coord]:
-            self.memory[coord] = elements
+        self.memory[coord] = max(self.memory[coord], elements)
 
+    def record_timing(self, label: str, device_ms: float, *, flops: float = 0.0, nbytes: float = 0.0,
+                      bound: str = "tensor", peak: float = 0.0, gpus: int = 1) -> None:
+        """One timed launch: device time (max over the GPUs that ran it) and
+        its algorithmic work, from which the measured rates follow."""
+        self.timings.append({"label": label, "device_ms": device_ms, "flops": flops, "bytes": nbytes,
+                             "bound": bound, "peak": peak, "gpus": gpus})
+
+    # -- queries ----------------------------------------------------------------
     @property
     def high_water(self) -> int:
         return max(self.memory.values(), default=0)
 
     def events_of(self, kind=None, phase=None, tensor=None, step=None) -> list:
-        want = {"kind": kind, "phase": phase, "tensor": tensor, "timestep": step}
-        want = {k: v for k, v in want.items() if v is not None}
-        return [e for e in self.events if all(getattr(e, k) == v for k, v in want.items())]
+        wanted = [(_FILTER_FIELDS[k], v) for k, v in
+                  (("kind", kind), ("phase", phase), ("tensor", tensor), ("step", step)) if v is not None]
+        return [e for e in self.events if all(getattr(e, f) == v for f, v in wanted)]
 
     @property
     def total_messages(self) -> int:
@@ -88,62 +121,73 @@ class ExecutionTrace:
         return sum(e.elements for e in self.events)
 
     def per_edge(self) -> list:
-        agg: dict = {}
-        for e in self.events:
-            m, n = agg.get((e.src, e.dst), (0, 0))
-            agg[(e.src, e.dst)] = (m + 1, n + e.elements)
-        rank = self.machine.rank_of
-        return [{"src": list(s), "dst": list(d), "messages": agg[(s, d)][0],
-                 "elements": agg[(s, d)][1]}
-                for s, d in sorted(agg, key=lambda sd: (rank(sd[0]), rank(sd[1])))]
+        groups = _rollup(self.events, key=lambda e: (e.src, e.dst))
+        order = sorted(groups, key=lambda edge: tuple(map(self.machine.rank_of, edge)))
+        return [{"src": list(src), "dst": list(dst), **_pair(groups[(src, dst)])} for src, dst in order]
 
     def per_step(self) -> list:
-        agg: dict = {}
-        for e in self.events:
-            if e.phase == "compute":
-                m, n = agg.get(e.timestep, (0, 0))
-                agg[e.timestep] = (m + 1, n + e.elements)
-        return [{"step": s, "messages": agg.get(s, (0, 0))[0], "elements": agg.get(s, (0, 0))[1]}
-                for s in range(self.num_steps)]
+        groups = _rollup(self.events_of(phase="compute"), key=lambda e: e.timestep)
+        return [{"step": s, **_pair(groups.get(s))} for s in range(self.num_steps)]
+
+    # -- stats ------------------------------------------------------------------
+    def _totals(self) -> dict:
+        by_kind = _rollup(self.events, key=lambda e: e.kind)
+        out = {"messages": self.total_messages, "elements": self.total_elements}
+        for kind in ("copy", "reduce"):
+            m, n = by_kind.get(kind, (0, 0))
+            out[f"{kind}_messages"], out[f"{kind}_elements"] = m, n
+        return out
+
+    def _phases(self) -> dict:
+        by_phase = _rollup(self.events, key=lambda e: e.phase)
+        return {ph: _pair(by_phase.get(ph)) for ph in ("placement", "compute")}
+
+    def _memory(self) -> dict:
+        return {"overall": self.high_water,
+                "per_processor": [{"processor": list(p), "elements": self.memory[p]}
+                                  for p in self.machine.enumerate()]}
+
+    def _levels(self):
+        if self.machine.num_levels <= 1:
+            return None
+        cut = self.machine.level_slices()[0][1]
+        split = _rollup(self.events, key=lambda e: e.src[:cut] == e.dst[:cut])
+        return {"intra_node": _pair(split.get(True)), "inter_node": _pair(split.get(False))}
+
+    def _measured(self):
+        if not self.timings:
+            return None
+        rows = []
+        for t in self.timings:
+            sec = t["device_ms"] * 1e-3
+            rate = (t["flops"] / sec / 1e9 if t["bound"] == "tensor" else t["bytes"] / sec / 1e9) if sec > 0 else 0.0
+            rows.append({**t, "rate": rate, "rate_unit": "GFLOP/s" if t["bound"] == "tensor" else "GB/s",
+                         "frac_of_peak": rate / (t["peak"] * t["gpus"]) if t["peak"] else None})
+        total_ms = sum(t["device_ms"] for t in self.timings)
+        return {"launches": rows, "device_ms": total_ms,
+                "flops": sum(t["flops"] for t in self.timings),
+                "bytes": sum(t["bytes"] for t in self.timings)}
+
+    _SECTIONS = (("totals", _totals), ("phases", _phases), ("per_edge", per_edge),
+                 ("per_step", per_step), ("memory_high_water", _memory))
 
     def stats(self, config=None) -> dict:
-        copies, reduces = self.events_of(kind="copy"), self.events_of(kind="reduce")
-        out = {
-            "schema": 1,
-            "config": dict(config or {}),
-            "machine": str(self.machine),
-            "num_steps": self.num_steps,
-            "totals": {
-                "messages": self.total_messages,
-                "elements": self.total_elements,
-                "copy_messages": len(copies),
-                "copy_elements": sum(e.elements for e in copies),
-                "reduce_messages": len(reduces),
-                "reduce_elements": sum(e.elements for e in reduces),
-            },
-            "phases": {"placement": _tally(self.events_of(phase="placement")),
-                       "compute": _tally(self.events_of(phase="compute"))},
-            "per_edge": self.per_edge(),
-            "per_step": self.per_step(),
-            "memory_high_water": {
-                "overall": self.high_water,
-                "per_processor": [{"processor": list(p), "elements": self.memory[p]}
-                                  for p in self.machine.enumerate()],
-            },
-            "launches": list(self.launches),
-        }
-        if self.machine.num_levels > 1:
-            cut = self.machine.level_slices()[0][1]
-            same = [e for e in self.events if e.src[:cut] == e.dst[:cut]]
-            cross = [e for e in self.events if e.src[:cut] != e.dst[:cut]]
-            out["levels"] = {"intra_node": _tally(same), "inter_node": _tally(cross)}
+        out = {"schema": 1, "config": dict(config or {}), "machine": str(self.machine),
+               "num_steps": self.num_steps}
+        for name, build in self._SECTIONS:
+            out[name] = build(self)
+        out["launches"] = list(self.launches)
+        for name, build in (("levels", ExecutionTrace._levels), ("measured", ExecutionTrace._measured)):
+            section = build(self)
+            if section is not None:
+                out[name] = section
         return out
 
 
 def write_edge_csv(trace: ExecutionTrace, path) -> None:
+    """Per-edge aggregate as CSV: src,dst,messages,elements."""
+    rows = [["src", "dst", "messages", "elements"]]
+    rows += [["x".join(map(str, r["src"])), "x".join(map(str, r["dst"])), r["messages"], r["elements"]]
+             for r in trace.per_edge()]
     with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(["src", "dst", "messages", "elements"])
-        for row in trace.per_edge():
-            w.writerow(["x".join(map(str, row["src"])), "x".join(map(str, row["dst"])),
-                        row["messages"], row["elements"]])
+        csv.writer(fh).writerows(rows)

@@ -67,3 +67,38 @@ def test_g1_real_within_gamma_of_the_reference():
     err = np.abs(got - ref)
     assert np.all(err <= 2 * gam * bound)
     assert np.all(err <= 1e-10 * n * bound)
+
+
+def test_g1_reference_contract_plugin_runs_unchanged():
+    """The drop-in boundary: a leaf written against the REFERENCE's plugin
+    contract (oracle/ref_leaf.py: host DenseTensors in global coordinates,
+    in-place writes into a full-size out_store; reference cin.py:359-379) is
+    registered with the plain `register_leaf_kernel(name, fn)` call and
+    substituted with `Schedule.substitute_leaf` exactly as on tendist -- and
+    reproduces the reference's own G1 output bit for bit."""
+    from oracle.ref_leaf import NAME, innermost_vars, numpy_leaf
+    td.register_leaf_kernel(NAME, numpy_leaf)
+    b = _bundle()
+    sched = b.schedule.substitute_leaf(innermost_vars(b.scheduled()), NAME)
+    ins = td.random_inputs(b.statement, 0)
+    res = td.run_statement(b.statement, b.machine, b.distributions, ins, sched)
+    assert _sha(res.output.data) == G1["int"]["output_sha256"]
+    assert len(res.trace.events) == G1["int"]["events"]
+
+
+@pytest.mark.parametrize("case", ["summa", "cannon", "johnson", "ttv", "mttkrp"])
+def test_reference_contract_plugin_on_bundles(case):
+    """Same host-contract plugin on other bundles (ragged shapes), against the
+    GPU's exact-order interpreter."""
+    from oracle.ref_leaf import NAME, innermost_vars, numpy_leaf
+    td.register_leaf_kernel(NAME, numpy_leaf)
+    b = {"summa": lambda: td.summa(2, 2, dims=(13, 11, 17), chunk=3),
+         "cannon": lambda: td.cannon(2, 2, dims=(10, 9, 7)),
+         "johnson": lambda: td.johnson(2, 2, 2, dims=(9, 7, 11)),
+         "ttv": lambda: td.ttv(3, dims=(7, 5, 6)),
+         "mttkrp": lambda: td.mttkrp(2, 2, dims=(6, 5, 7, 3))}[case]()
+    ins = td.random_inputs(b.statement, 11)
+    sched = b.schedule.substitute_leaf(innermost_vars(b.scheduled()), NAME)
+    got = td.run_statement(b.statement, b.machine, b.distributions, ins, sched).output.data
+    want = td.sequential_evaluate(b.statement, ins).data
+    assert np.array_equal(got, want)

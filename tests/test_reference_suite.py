@@ -1,11 +1,13 @@
 """Drop-in check: the REFERENCE's own unit tests, run against this package.
 
-When the reference checkout is present (the build container), every test
-module of `pkg/tests` except the CLI ones is loaded with `tendist` and its
+The reference's own tests are staged by `make ref` into oracle/_ref/tests
+(git-ignored, travels to the GPU box with the snapshot; read in place, never
+committed).  Every test module except the CLI ones is loaded with `tendist` and its
 submodules aliased to `paper_2203_08069_b200`, and each test function is run
 unmodified.  Tests that need values computed (run_statement, interpret,
 sequential_evaluate) raise DeviceUnavailable on a GPU-less host and are
-reported as skipped; everything else -- machines, tensors and their file
+reported as skipped there; the `-m gpu` twin runs every case on the B200
+and fails on DeviceUnavailable; everything else -- machines, tensors and their file
 formats, the IR and parser, CIN structure and pretty-printing, distributions,
 the scheduling language and its error taxonomy -- must pass as is.
 Nothing is copied from the reference: its test files are read in place.
@@ -18,7 +20,9 @@ import sys
 
 import pytest
 
-REF_TESTS = "/root/reference/pkg/tests"
+from oracle.reference import tests_dir
+
+REF_TESTS = tests_dir()
 SKIP_FILES = {"test_cli.py", "test_acceptance.py"}    # exercise the reference CLI (out of scope)
 
 
@@ -42,7 +46,7 @@ def _restore(saved):
 
 
 def _collect():
-    if not os.path.isdir(REF_TESTS):
+    if not REF_TESTS:
         return []
     saved = _alias()
     cases = []
@@ -72,11 +76,10 @@ def _collect():
 CASES = _collect()
 
 
-@pytest.mark.skipif(not CASES, reason="reference checkout not present")
-@pytest.mark.parametrize("case", CASES, ids=[f"{c[0][:-3]}::{c[1]}" for c in CASES] or None)
-def test_reference_unit_test(case, tmp_path, capsys, monkeypatch):
+def _run(case, tmp_path, capsys, monkeypatch, on_gpu):
     from paper_2203_08069_b200.errors import DeviceUnavailable
     fname, name, fn, kwargs = case
+    kwargs = dict(kwargs)
     fixtures = {"tmp_path": tmp_path, "capsys": capsys, "monkeypatch": monkeypatch}
     wanted = inspect.signature(fn).parameters
     for p in wanted:
@@ -88,6 +91,25 @@ def test_reference_unit_test(case, tmp_path, capsys, monkeypatch):
     try:
         fn(**kwargs)
     except DeviceUnavailable:
-        pytest.skip("computes values: runs on the GPU (see the -m gpu parity tests)")
+        if on_gpu:
+            raise
+        pytest.skip("computes values: runs on the GPU (test_reference_unit_test_on_b200)")
     finally:
         _restore(saved)
+
+
+IDS = [f"{c[0][:-3]}::{c[1]}" for c in CASES] or None
+
+
+@pytest.mark.skipif(not CASES, reason="reference tests not staged (make ref)")
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_reference_unit_test(case, tmp_path, capsys, monkeypatch):
+    _run(case, tmp_path, capsys, monkeypatch, on_gpu=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not CASES, reason="reference tests not staged (make ref)")
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_reference_unit_test_on_b200(case, tmp_path, capsys, monkeypatch):
+    """The same unmodified reference test, values computed by the B200 path."""
+    _run(case, tmp_path, capsys, monkeypatch, on_gpu=True)
