@@ -24,8 +24,11 @@ GPU (GB/s vs HBM), TTM 1024^3 x 64 and MTTKRP 1024^3 rank 32 per GPU
 
 Under torchrun (WORLD_SIZE > 1) every rank drives its GPU; times are
 max-over-ranks of CUDA-event measurements bracketed by barriers.
-`--impl reference` times the reference algorithm's CPU port
-(oracle/distributed.py, numpy/OpenBLAS on all host cores) on rank 0.
+`--impl reference` times the REFERENCE itself on rank 0: tendist (staged
+in oracle/_ref) running the same GEMM bundle through its own
+`run_statement`, with a numpy/OpenBLAS leaf substituted through its plugin
+API (oracle/ref_bench.py), at the same n on all host cores; plus CPU-A, the
+reference as shipped (per-point interpreter, one core) at a scaled shape.
 """
 
 from __future__ import annotations
@@ -492,57 +495,115 @@ def bench_kernels(job, steps, warmup):
 
 
 # ------------------------------------------------------------------ CPU side
-def cpu_gemm(p, n=4096, reps=2):
-    """oracle/distributed.py's port of the reference algorithm at a bounded n
-    (integer-valued inputs in [-4, 4]: numpy's generator above 4096, where the
-    splitmix twin would take longer than the product)."""
-    from oracle import distributed as port
-    from oracle.generator import generate
-    if n > 4096:
-        rng = np.random.default_rng(0)
-        a = rng.integers(-4, 5, size=(n, n), dtype=np.int8).astype(np.float64)
-        b = rng.integers(-4, 5, size=(n, n), dtype=np.int8).astype(np.float64)
-    else:
-        a, b = generate((n, n), 0, 1, 0), generate((n, n), 0, 2, 0)
-    port.gemm_for_gpus(p, a[:256, :256].copy(), b[:256, :256].copy())
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        c = port.gemm_for_gpus(p, a, b)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    assert np.array_equal(c[:2], a[:2] @ b)
-    return 2.0 * n ** 3 / best / 1e9, best
+def _ints(n, seed):
+    """n x n integer-valued fp64 in [-4, 4] (numpy's fast generator: the
+    reference arm's inputs only need the right shape and value range)."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(-4, 5, size=(n, n), dtype=np.int8).astype(np.float64)
 
 
-def run_reference(args):
+def _host_ram_fits(n, tasks) -> bool:
+    """Can tendist's run_statement hold n^2 GEMM operands in host RAM?  It
+    keeps the caller's inputs, its placed copies (simulator.py:303), one
+    full-size zeroed output per task alive at once (cin.py:441-446) and the
+    canonical output."""
+    import psutil
+    need = 8.0 * n * n * (4 + tasks + 1)
+    return need < 0.85 * psutil.virtual_memory().available
+
+
+def reference_gemm(p, steps, n=None):
+    """The REFERENCE (tendist from oracle/_ref) on the headline GEMM of p GPUs:
+    its own run_statement with the numpy/BLAS leaf substituted through its
+    plugin API (oracle/ref_bench.py), at the full headline n when host RAM
+    allows (else the largest multiple of 256 that fits, stated)."""
+    import paper_2203_08069_b200 as td
+    from oracle.ref_bench import blas_threads, run_reference
+    full = td.weak_gemm_n(p)
+    bundle = td.gemm_for_gpus(p, full)
+    tasks = bundle.machine.size
+    n = n or full
+    while not _host_ram_fits(n, tasks) and n > 1024:
+        n -= 256 * max(1, n // 4096)
+    bundle = td.gemm_for_gpus(p, n)
+    a, b = _ints(n, 1), _ints(n, 2)
+    ins = {"A": td.DenseTensor((n, n), a), "B": td.DenseTensor((n, n), b)}
+    times = []
+    out = None
+    for _ in range(steps):
+        out, secs, _ = run_reference(bundle, ins)
+        times.append(secs)
+    rows = [0, n // 2, n - 1]
+    ok = bool(np.array_equal(out[rows], a[rows] @ b))
+    secs = statistics.median(times)
+    del out, ins, a, b
+    gc.collect()
+    return {"value": 2.0 * n ** 3 / secs / 1e9, "secs": secs, "n": n, "same_shape": n == full,
+            "cores": blas_threads(), "rows_exact": ok,
+            "sample": f"tendist run_statement ({bundle.name} on {bundle.machine}, n={n}"
+                      f"{'' if n == full else f'; the headline n={full} does not fit host RAM'}) with a numpy/"
+                      f"OpenBLAS leaf substituted through its own plugin API (register_leaf_kernel + "
+                      f"substitute_leaf; oracle/ref_bench.py), {blas_threads()} BLAS threads, median of "
+                      f"{steps} run(s), inputs placed by run_statement inside the timing"}
+
+
+def reference_interpreter_rate(p):
+    """CPU-A: the reference AS SHIPPED (its per-point Python interpreter leaf,
+    workers=1 -> one core) on the headline algorithm at a scaled shape."""
+    import paper_2203_08069_b200 as td
+    from oracle.ref_bench import run_reference
+    n = 32
+    bundle = td.gemm_for_gpus(p, n)
+    _, secs, _ = run_reference(bundle, leaf="interpreter")
+    pts = float(n) ** 3
+    return {"value": 2.0 * pts / secs / 1e6, "unit": "MFLOP/s", "kpoints_per_s": pts / secs / 1e3, "cores": 1,
+            "sample": f"tendist run_statement as shipped (per-point interpreter) {bundle.name} on {bundle.machine}, "
+                      f"n={n}", "full_shape_hours": 2.0 * td.weak_gemm_n(p) ** 3 / (2.0 * pts / secs) / 3600}
+
+
+def reference_kernels():
+    """cpu_baseline of the other BASELINE configs: the reference + numpy leaf
+    at scaled shapes (the full ones exceed host RAM / minutes of CPU)."""
+    import paper_2203_08069_b200 as td
+    from oracle.ref_bench import blas_threads, run_reference
+    out = {}
+    m = 512
+    cases = [("ttv_2048", td.ttv(1, dims=(m, m, m)), 8.0 * (m ** 3 + m + m * m), "GB/s"),
+             ("innerprod3_2048", td.innerprod3(1, dims=(m, m, m)), 16.0 * m ** 3, "GB/s"),
+             ("ttm_1024_64", td.ttm2d(1, 1, dims=(m, m, m, 64)), 2.0 * m ** 3 * 64, "GFLOP/s"),
+             ("mttkrp_1024_r32", td.mttkrp(1, 1, dims=(m, 32, m, m)), 2.0 * m ** 3 * 32 + 2.0 * m * m * 32,
+              "GFLOP/s")]
+    for name, bundle, work, unit in cases:
+        run_reference(bundle)   # warm
+        _, secs, _ = run_reference(bundle)
+        out[name] = {"value": work / secs / 1e9, "unit": unit, "cores": blas_threads(), "kind": "reference",
+                     "sample": f"tendist run_statement + numpy leaf, {bundle.name} on {bundle.machine} at "
+                               f"{m}^3 ({secs:.2f} s)"}
+    return out
+
+
+def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import paper_2203_08069_b200 as td
     p = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
-    cores = os.cpu_count()
-    n = 8192
+    # warm-up: the same code path at a small shape (BLAS threads, imports)
     for _ in range(max(0, args.warmup)):
-        cpu_gemm(p, n=1024, reps=1)
-    vals = []
+        reference_gemm(p, steps=1, n=1024)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, _ = cpu_gemm(p, n=n, reps=1)
-        vals.append(v)
+    r = reference_gemm(p, steps=args.steps)
     wall = time.perf_counter() - t0
-    value = statistics.median(vals)
-    import paper_2203_08069_b200 as td  # names only (no GPU use)
-    nfull = td.weak_gemm_n(p)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": p,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"fp64 GEMM weak-scaled (n={nfull} at {p} GPU(s)); CPU sample n={n} with the same "
-                               f"algorithm ({td.gemm_for_gpus(p, 64).name}, {td.gemm_for_gpus(p, 64).machine})"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle/distributed.py {td.gemm_for_gpus(p, 64).name} at n={n}, numpy/OpenBLAS, "
-                                   f"{cores} threads; the reference's own per-point interpreter runs ~1e5 points/s"},
-        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GFLOP/s", "n_gpus": p,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["secs"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": gemm_config(td, p) if r["same_shape"] else {**gemm_config(td, p), "cpu_n": r["n"]},
+        "cpu_baseline": {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
+                         "sample": r["sample"], "rows_exact": r["rows_exact"]},
+        "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_a": reference_interpreter_rate(p),
+        "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
 
@@ -559,7 +620,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference_arm(args)
         return
     job = Job(args.gpus)
     gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps)
@@ -569,24 +630,33 @@ def main():
     job.close()
 
 
+def gemm_config(td, p):
+    """The headline workload's `config` -- identical in both arms."""
+    n = td.weak_gemm_n(p)
+    b = td.gemm_for_gpus(p, n)
+    return {"workload": f"fp64 GEMM {n}^3 weak-scaled from 16384^3 ({b.name} on {b.machine})", "n": n,
+            "algorithm": b.name, "grid": str(b.machine), "parallelism": f"{p} GPU(s), one task per GPU",
+            "l2": "inputs (>= 2 GiB per operand) exceed the 126 MB L2; no flush needed",
+            "inputs": "integer-valued fp64 in [-4,4]"}
+
+
 def report(args, job, gemm, kernels):
     cpu = None
     if job.n_gpus == 1 and not args.no_cpu_baseline:
-        # the headline workload itself (16384^3, ~10 s on the box's cores), one timed run
-        v, secs = cpu_gemm(1, n=16384, reps=1)
-        cpu = {"value": v, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"oracle/distributed.py cannon 1x1 at n=16384 (the headline shape; {secs:.1f} s), "
-                         "numpy/OpenBLAS on all host cores"}
+        # the reference itself on the headline workload (16384^3, ~10 s on the box's cores), one run
+        r = reference_gemm(1, steps=1)
+        cpu = {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
+               "sample": r["sample"], "rows_exact": r["rows_exact"]}
+        if kernels:
+            for name, cb in reference_kernels().items():
+                if name in kernels:
+                    kernels[name]["cpu_baseline"] = cb
     p = job.n_gpus
     line = {
         "metric": METRIC, "value": gemm["value"], "unit": "GFLOP/s", "n_gpus": p, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": gemm["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"fp64 GEMM {gemm['n']}^3 weak-scaled from 16384^3 ({gemm['bundle']} on "
-                               f"{gemm['machine']})", "n": gemm["n"], "algorithm": gemm["bundle"],
-                   "grid": gemm["machine"], "parallelism": f"{p} GPU(s), one task per GPU",
-                   "l2": "inputs (>= 2 GiB per operand) exceed the 126 MB L2; no flush needed",
-                   "inputs": "integer-valued fp64 in [-4,4] from the device generator (oracle/generator.py twin)"},
+        "config": gemm_config(job.td, p),
         "per_gpu": gemm["per_gpu"], "check": gemm["check"], "roofline": gemm["roofline"],
         "cpu_baseline": cpu, "e2e": gemm["e2e"], "gpu_launches": gemm["gpu_launches"],
         "gpu_launches_per_step": gemm["launches_per_step"], "clocks": gemm["clocks"],
