@@ -418,6 +418,31 @@ def bench_gemm_e2e(job, bundle, cin, steps):
                    "host wall clock, max over ranks"}
 
 
+def _spot_check(job, bundle, store, per_piece=4):
+    """Result check of a timed config on every rank: sampled points of this
+    rank's output pieces against the exact integer value recomputed on the
+    host from the generated input slices (oracle/spot.py; integer inputs, so
+    the comparison is bit-exact).  Scalar outputs (innerprod) are checked in
+    tests/test_fullsize_gpu.py instead (the host total takes minutes)."""
+    from oracle.spot import points
+    stmt = bundle.statement
+    out = stmt.lhs.tensor.name
+    if not stmt.lhs.var_names:
+        return {"points": 0, "exact": None, "note": "scalar output: tests/test_fullsize_gpu.py"}
+    rng = np.random.default_rng(job.rank)
+    coords, got = [], []
+    for box, buf in store.local_pieces(out):
+        for k in range(per_piece):
+            c = tuple(int(lo if k == 0 else hi - 1 if k == 1 else rng.integers(lo, hi))
+                      for lo, hi in zip(box.lo, box.hi))
+            coords.append(c)
+            got.append(float(buf[tuple(x - lo for x, lo in zip(c, box.lo))].item()))
+    bad = sum(1 for g, (e, _, _) in zip(got, points(stmt, coords, seed=0, mode=0)) if g != e)
+    npts = job.sum_over_ranks(float(len(coords)))
+    nbad = job.sum_over_ranks(float(bad))
+    return {"points": int(npts), "exact": nbad == 0}
+
+
 # ------------------------------------------------------------------ other configs
 def bench_kernels(job, steps, warmup):
     td, torch = job.td, job.torch
@@ -444,6 +469,7 @@ def bench_kernels(job, steps, warmup):
         ms = job.timed(step, nsteps, 0)
         kms, nk = _leaf_timing(td, kind)
         leaves.TIMING = None
+        check = _spot_check(job, bundle, store)
         per_gpu_work = work / p
         rate = work * nsteps / (ms / 1e3) / 1e9
         kern = per_gpu_work / (kms / 1e3) / 1e9 if kms else None
@@ -452,7 +478,7 @@ def bench_kernels(job, steps, warmup):
                 tuple(bundle.statement.extents[v] for v in bundle.statement.var_order)),
             "value": rate, "unit": unit, "per_gpu": rate / p, "ms_per_step": ms / nsteps, "steps": nsteps,
             "kernel": kind, "kernel_ms": kms, "kernel_rate_per_gpu": kern,
-            "frac_of_roof": (kern / roof) if kern else None, "roof": roof,
+            "frac_of_roof": (kern / roof) if kern else None, "roof": roof, "check": check,
         }
         del store, step
         gc.collect()

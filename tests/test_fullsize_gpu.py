@@ -114,3 +114,96 @@ def test_mttkrp_1024_r32_sampled_rows():
         bi = generate_box((m, m, m), (i, 0, 0), (1, m, m), 0, 1, 0)[0]
         want = ((bi @ dm) * cm).sum(axis=0)
         assert np.array_equal(a[i].cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- real-valued, full size
+# uniform(-1, 1) inputs (generator mode 1): sampled output points against a
+# long-double evaluation of the same generated slices (oracle/spot.py).  Two
+# bounds, both written here: the rounding-error bound |got - exact| <=
+# gamma_n * sum|products| (n = reduction length + product depth, u = 2^-53),
+# and the north star's "1e-10 scaled by the reduction length" relative to the
+# same magnitude.
+def _point_values(store, name, coords):
+    got = []
+    pieces = list(store.local_pieces(name))
+    for c in coords:
+        for box, buf in pieces:
+            if all(a <= x < b for x, a, b in zip(c, box.lo, box.hi)):
+                got.append(float(buf[tuple(x - a for x, a in zip(c, box.lo))].item()))
+                break
+        else:
+            raise AssertionError(f"{name}{c} is not resident")
+    return got
+
+
+def _check_real(bundle, depth, seed=3):
+    from oracle.spot import gamma, points, reduction_length
+    torch.cuda.empty_cache()
+    cin, store = bundle.prepare(seed=seed, mode=1)
+    td.execute(cin, store)
+    stmt = bundle.statement
+    out = stmt.lhs.tensor.name
+    dims = stmt.lhs.tensor.dims
+    rng = np.random.default_rng(seed)
+    coords = [tuple(0 for _ in dims), tuple(d - 1 for d in dims)]
+    coords += [tuple(int(rng.integers(0, d)) for d in dims) for _ in range(6)]
+    got = _point_values(store, out, coords)
+    k = reduction_length(stmt)
+    g = gamma(k + depth)
+    for c, x, (_, exact, bound) in zip(coords, got, points(stmt, coords, seed=seed, mode=1)):
+        err = abs(np.longdouble(x) - exact)
+        assert err <= g * bound, (c, float(err), float(g * bound))
+        assert err <= 1e-10 * k * bound, (c, float(err))
+    del store
+    torch.cuda.empty_cache()
+
+
+def test_real_gemm_16384_within_gamma():
+    n = 16384
+    _check_real(td.cannon(1, 1, dims=(n, n, n)), depth=1)
+
+
+def test_real_ttv_2048_within_gamma():
+    n = 2048
+    _check_real(td.ttv(1, dims=(n, n, n)), depth=1)
+
+
+def test_real_ttm_1024x64_within_gamma():
+    m = 1024
+    _check_real(td.ttm2d(1, 1, dims=(m, m, m, 64)), depth=1)
+
+
+def test_real_mttkrp_1024_r32_within_gamma():
+    m = 1024
+    _check_real(td.mttkrp(1, 1, dims=(m, 32, m, m)), depth=2)
+
+
+def test_innerprod_2048_total_exact_against_host():
+    """The full 2 x 2048^3 inner product (137 GB in HBM) against an exact
+    integer total computed independently on the host from the generator,
+    slab by slab on every host core (oracle/host_totals.py)."""
+    from oracle.host_totals import innerprod_total
+    n = 2048
+    torch.cuda.empty_cache()
+    b = td.innerprod3(1, dims=(n, n, n))
+    cin, store = b.prepare(seed=4, mode=0)
+    td.execute(cin, store)
+    got = store.gather("a").data.item()
+    del store
+    torch.cuda.empty_cache()
+    want, _ = innerprod_total((n, n, n), 4, (1, 2), 0)
+    assert got == float(want) and abs(want) < 2 ** 53
+
+
+def test_real_innerprod_1024_within_gamma():
+    from oracle.host_totals import innerprod_total
+    from oracle.spot import gamma
+    n = 1024
+    b = td.innerprod3(1, dims=(n, n, n))
+    cin, store = b.prepare(seed=5, mode=1)
+    td.execute(cin, store)
+    got = np.longdouble(store.gather("a").data.item())
+    want, absum = innerprod_total((n, n, n), 5, (1, 2), 1)
+    k = n ** 3
+    assert abs(got - want) <= gamma(k + 1) * absum
+    assert abs(got - want) <= 1e-10 * k * absum
