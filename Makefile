@@ -9,7 +9,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr \
              -I$(NCCL_ROOT)/include -Iinclude
 LDFLAGS   := -shared -L$(NCCL_ROOT)/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_ROOT)/lib -cudart static
-SRCS      := $(CSRC)/capi.cu $(CSRC)/gemm.cu $(CSRC)/mttkrp.cu $(CSRC)/stream.cu $(CSRC)/interp.cu $(CSRC)/comm.cu $(CSRC)/peer.cu
+SRCS      := $(CSRC)/capi.cu $(CSRC)/gemm.cu $(CSRC)/mttkrp.cu $(CSRC)/stream.cu $(CSRC)/interp.cu $(CSRC)/comm.cu $(CSRC)/peer.cu $(CSRC)/plan.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB       := $(PKG)/libdistal_b200.so
 

@@ -74,6 +74,25 @@ int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t 
                      const double* B, int64_t ldb, int64_t strideB,
                      double* C, int64_t ldc, int64_t strideC, int accumulate);
 
+/* Grouped GEMM: `count` (<= TD_GEMM_GROUP_MAX) independent GEMMs of any
+ * shapes in ONE launch (the tiles of all problems share the grid).  Used for
+ * the same-step GEMM leaves of the tasks co-located on one GPU (reference
+ * simulator.py:615-622 runs them one after another): every output element
+ * gets exactly the arithmetic of a separate td_dgemm call.  `problems` is
+ * read during the call only.  Falls back to per-problem launches when a
+ * problem cannot be addressed by TMA. */
+#define TD_GEMM_GROUP_MAX 8
+typedef struct td_gemm_problem {
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+} td_gemm_problem;
+int td_dgemm_grouped(void* stream, int count, const td_gemm_problem* problems, int accumulate);
+
 /* TTV leaf  A(i,j) (+)= sum_k B(i,j,k) * c(k)   -- algorithms.py:280-281.
  * Rows (i,j) with element strides (sBi, sBj) in B and (sAi, sAj) in A; k
  * stride of B and c is 1.  Bandwidth-bound: 128-bit loads, one warp per row,
@@ -190,6 +209,37 @@ int td_peer_free(int device, void* ptr);
 /* Map another process's td_peer_alloc buffer into `device`'s context. */
 int td_peer_open(int device, const char* ipc_handle, void** ptr);
 int td_peer_close(int device, void* ptr);
+
+/* ---- launch plans: the per-step loop in one call (csrc/plan.cu) ----------
+ * One launch of a scheduled statement (reference simulator.py:557-663: per
+ * step the fetches, every task's leaf, then the commits) lowered to a flat
+ * array of ops in issue order.  Each op names one entry point of this header
+ * and carries its arguments, in order, as 64-bit words (pointers and
+ * integers as-is, doubles bit-cast); arrays an op points to (copy_box
+ * shapes/strides, nest programs, grouped-GEMM problems) must outlive the
+ * plan.  td_execute_plan issues every op, stops at the first failure (its
+ * index in td_last_error(); an open NCCL group is closed), and is
+ * asynchronous like the calls it replays. */
+enum {
+  TD_OP_DGEMM = 1, TD_OP_DGEMM_BATCHED = 2, TD_OP_DGEMM_GROUPED = 3, TD_OP_TTV = 4, TD_OP_TTM = 5,
+  TD_OP_MTTKRP = 6, TD_OP_INNERPROD = 7, TD_OP_NEST_EVAL = 8, TD_OP_COPY_BOX = 9, TD_OP_MEMCPY_2D = 10,
+  TD_OP_FILL = 11, TD_OP_GROUP_START = 12, TD_OP_GROUP_END = 13, TD_OP_SEND = 14, TD_OP_RECV = 15,
+  TD_OP_BCAST = 16, TD_OP_REDUCE_SUM = 17, TD_OP_EVENT_RECORD = 18, TD_OP_STREAM_WAIT = 19
+};
+#define TD_OP_MAX_ARGS 16
+typedef struct td_op {
+  int32_t kind;
+  int32_t nargs;
+  int64_t arg[TD_OP_MAX_ARGS];
+} td_op;
+int td_execute_plan(const td_op* ops, int64_t count);
+
+/* Cross-stream edges of a plan (no timing): record on the producer stream,
+ * wait on the consumer stream. */
+int td_event_create(int device, void** event);
+int td_event_destroy(void* event);
+int td_event_record(void* event, void* stream);
+int td_stream_wait_event(void* stream, void* event);
 
 #ifdef __cplusplus
 }

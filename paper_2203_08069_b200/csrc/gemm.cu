@@ -19,8 +19,10 @@
 // K or N not a multiple of 4, unaligned bases).
 // Summation order: k tiles ascending, within a tile the DMMA's own order --
 // exact on integer-valued data, |err| <= gamma_K |A||B| on real data.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "dmma.cuh"
@@ -558,6 +560,38 @@ int td_dgemm_batched(void* stream, int64_t batch, int64_t M, int64_t N, int64_t 
     done += chunk;
   }
   return TD_OK;
+}
+
+int td_dgemm_grouped(void* stream, int count, const td_gemm_problem* problems, int accumulate) {
+  TD_REQUIRE(count >= 0 && count <= TD_GEMM_GROUP_MAX && (count == 0 || problems),
+             "dgemm_grouped: 0..%d problems", TD_GEMM_GROUP_MAX);
+  td::StreamDevice sd(stream);
+  td::GemmArgs args[TD_GEMM_GROUP_MAX];
+  int n = 0;
+  bool tma = true;
+  int64_t maxN = 0;
+  for (int q = 0; q < count; ++q) {
+    const td_gemm_problem& pr = problems[q];
+    td::GemmArgs a{pr.M, pr.N, pr.K, pr.A, pr.lda, 0, pr.B, pr.ldb, 0, pr.C, pr.ldc, 0, accumulate, 0, 0, 0,
+                   nullptr, 0};
+    if (a.M <= 0 || a.N <= 0) continue;
+    if (a.K <= 0) {  // nothing to multiply: only the Assign form writes zeros
+      if (int rc = td::dgemm_dispatch(td::as_stream(stream), 1, a)) return rc;
+      continue;
+    }
+    tma = tma && td::tma_ok(1, a);
+    maxN = std::max(maxN, a.N);
+    args[n++] = a;
+  }
+  if (n == 0) return TD_OK;
+  if (!tma || n == 1) {  // one problem, or one TMA cannot address: separate launches
+    for (int q = 0; q < n; ++q)
+      if (int rc = td::dgemm_dispatch(td::as_stream(stream), 1, args[q])) return rc;
+    return TD_OK;
+  }
+  // the default TMA tiles (config 47 / 48 by N, gemm.cu default_tma_config)
+  if (maxN <= 32) return td::launch_gemm_tma_grouped<128, 32, 16, 32, 32, 3, 4>(td::as_stream(stream), n, args);
+  return td::launch_gemm_tma_grouped<64, 64, 16, 32, 32, 3, 4>(td::as_stream(stream), n, args);
 }
 
 int td_ttm(void* stream, int64_t I, int64_t J, int64_t K, int64_t L, const double* B, int64_t sBi,

@@ -63,19 +63,23 @@ struct TmaCfg {
   static_assert(BK % 4 == 0 && BN % 8 == 0 && BM <= 256 && BK * BN / 4 <= 256 * 64, "tma tile");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB = 0>
-__global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
-                                  TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
-dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+// One CTA tile of the TMA-fed GEMM: tile `tile` (raster order) of batch
+// entry `bz`, operands through the tensor maps tmA / tmB (kernel-parameter
+// addresses: __grid_constant__).  Shared by the plain kernel and the
+// grouped one below.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB>
+__device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUtensorMap* tmB_, const GemmArgs& p,
+                                              const int tile, const int bz) {
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   extern __shared__ __align__(128) unsigned char tma_smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES];
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 127) & ~uintptr_t(127));
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
+  const CUtensorMap& tmA = *tmA_;
+  const CUtensorMap& tmB = *tmB_;
 
   // grouped rasterisation (as dgemm_kernel)
-  const int tile = blockIdx.x;
   const int per_group = p.group * p.tiles_n;
   const int first_m = (tile / per_group) * p.group;
   const int gsize = min(p.tiles_m - first_m, p.group);
@@ -84,7 +88,6 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int tn = in_g / gsize;
   const int m0 = tm * BM;
   const int n0 = tn * BN;
-  const int bz = blockIdx.y;
   const int bzB = p.sB ? bz : 0;
   double* __restrict__ C = p.C + int64_t(bz) * p.sC;
   const int64_t M = p.M, N = p.N, K = p.K;
@@ -209,6 +212,33 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB = 0>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
+                                  TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
+dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+  tma_gemm_tile<BM, BN, BK, WM, WN, STAGES, EPI, MINB>(&tmA, &tmB, p, blockIdx.x, blockIdx.y);
+}
+
+// Grouped launch: up to TD_GEMM_GROUP_MAX problems, their tiles laid end to
+// end along grid.x (problem q owns tiles [start[q], start[q+1])).
+struct alignas(64) GroupedTma {
+  CUtensorMap map[2 * TD_GEMM_GROUP_MAX];
+  GemmArgs args[TD_GEMM_GROUP_MAX];
+  int start[TD_GEMM_GROUP_MAX + 1];
+  int count;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
+                                  TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
+dgemm_tma_grouped_kernel(const __grid_constant__ GroupedTma g) {
+  const int x = blockIdx.x;
+  int q = 0;
+  while (q + 1 < g.count && x >= g.start[q + 1]) ++q;
+  const GemmArgs p = g.args[q];
+  tma_gemm_tile<BM, BN, BK, WM, WN, STAGES, 0, MINB>(&g.map[2 * q], &g.map[2 * q + 1], p, x - g.start[q], 0);
+}
+
 // ---- host side: tensor maps through the driver entry point (no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -262,6 +292,38 @@ static int launch_gemm_tma(cudaStream_t st, int64_t batch, GemmArgs a) {
   dim3 grid((unsigned)tiles, (unsigned)batch);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ma, mb, a);
   return check_launch("dgemm_tma_kernel");
+}
+
+}  // namespace td
+
+namespace td {
+
+// Grouped form of launch_gemm_tma (plain epilogue, batch 1 per problem).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
+static int launch_gemm_tma_grouped(cudaStream_t st, int count, const GemmArgs* probs) {
+  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
+  auto kern = dgemm_tma_grouped_kernel<BM, BN, BK, WM, WN, STAGES, MINB>;
+  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  GroupedTma g;
+  std::memset(&g, 0, sizeof g);
+  g.count = count;
+  int64_t tiles = 0;
+  for (int q = 0; q < count; ++q) {
+    GemmArgs a = probs[q];
+    if (int rc = make_sliced_map(&g.map[2 * q], a.A, a.M, a.K, a.lda, 1, 0, BM, BK)) return rc;
+    if (int rc = make_sliced_map(&g.map[2 * q + 1], a.B, a.K, a.N, a.ldb, 1, 0, BK, BN)) return rc;
+    a.tiles_m = (int)ceil_div(a.M, BM);
+    a.tiles_n = (int)ceil_div(a.N, BN);
+    a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);
+    g.args[q] = a;
+    g.start[q] = (int)tiles;
+    tiles += int64_t(a.tiles_m) * a.tiles_n;
+  }
+  g.start[count] = (int)tiles;
+  TD_REQUIRE(tiles < (1ll << 31), "dgemm_grouped: grid too large (%lld tiles)", (long long)tiles);
+  if (tiles == 0) return TD_OK;
+  kern<<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(g);
+  return check_launch("dgemm_tma_grouped_kernel");
 }
 
 }  // namespace td

@@ -254,6 +254,26 @@ def run_nest(loops, leaf, defs, out_tile, in_tiles, stream) -> None:
 
 
 # ------------------------------------------------------- single-memory API
+def device_buffer(shape, device, stream=None, *, zero: bool = False):
+    """float64 HBM buffer for a launch's temporaries.  While a launch plan is
+    being recorded (`_native.recording`) the buffer is kept alive by the plan
+    (its ops hold raw pointers into it), and a zero fill is a plan op
+    (td_fill) so replays zero it again."""
+    torch = torch_mod()
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            t = torch.empty(tuple(shape), dtype=torch.float64, device=device)
+    else:
+        t = torch.empty(tuple(shape), dtype=torch.float64, device=device)
+    rec = _native.recorder()
+    if rec is not None:
+        rec.hold(t)
+    if zero and t.numel():
+        st = stream if stream is not None else torch.cuda.current_stream(t.device)
+        _native.call("td_fill", stream_handle(st), C.c_void_p(t.data_ptr()), t.numel(), 0.0)
+    return t
+
+
 def _upload(name, t: DenseTensor, device):
     torch = torch_mod()
     data = torch.from_numpy(t.data).to(device)

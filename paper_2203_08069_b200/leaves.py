@@ -39,7 +39,7 @@ import numpy as np
 from . import _native
 from .cin import Divide, Reduce, Split
 from .errors import ConfigError, TendistError
-from .interp import DeviceTile, run_nest, stream_handle, torch_mod
+from .interp import DeviceTile, device_buffer, run_nest, stream_handle, torch_mod
 from .ir import Access, Mul, accesses_of
 from .distribution import HyperRect
 
@@ -298,8 +298,7 @@ def _packed(view, names, order, ext, stream):
     """Contiguous copy of `view` with its axes permuted into `order`."""
     torch = torch_mod()
     shape = [ext[v] for v in order]
-    with torch.cuda.stream(stream):
-        buf = torch.empty(shape, dtype=torch.float64, device=view.data.device)
+    buf = device_buffer(shape, view.data.device, stream)
     st = dict(zip(names, view.strides()))
     if shape:
         _native.call("td_copy_box", stream_handle(stream), len(order), _native.i64_array(shape),
@@ -365,8 +364,7 @@ def _contract(out_names, p_names, q_names, o, pv, qv, ext, stream, accumulate):
     if direct_out:
         optr, ostr, acc = o.ptr(), go, accumulate
     else:
-        with torch.cuda.stream(stream):
-            scratch = torch.empty((Bt, Mt, Nt), dtype=torch.float64, device=o.data.device)
+        scratch = device_buffer((Bt, Mt, Nt), o.data.device, stream)
         keep.append(scratch)
         optr, ostr, acc = scratch.data_ptr(), [Mt * Nt, Nt, 1], 0
     lda = gp[1] if mvars else Kt
@@ -422,9 +420,7 @@ def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate
     rb, rc = _rows_view(b), _rows_view(c)
     if rb is None or rc is None or rb[:2] != rc[:2]:
         return False
-    torch = torch_mod()
-    work = torch.empty(int(_native.lib().td_innerprod_work_size()), dtype=torch.float64,
-                       device=out.data.device)
+    work = device_buffer((int(_native.lib().td_innerprod_work_size()),), out.data.device, stream)
     _native.call("td_innerprod", stream_handle(stream), rb[0], rb[1], _p(b), rb[2], _p(c), rc[2],
                  _p(out), C.c_void_p(work.data_ptr()), accumulate)
     if stream is not None:
@@ -435,6 +431,9 @@ def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate
 def _timing_start(stream):
     if TIMING is None:
         return None
+    rec = _native.recorder()
+    if rec is not None:
+        rec.invalidate("leaf timing is on")
     torch = torch_mod()
     ev = torch.cuda.Event(enable_timing=True)
     ev.record(stream)

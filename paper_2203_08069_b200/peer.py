@@ -156,6 +156,7 @@ class InboxSet:
     def __init__(self, prog, world, gpu_of):
         self.prog = prog
         self.inboxes = {}
+        self.pins = 0          # captured graphs / recorded plans holding raw inbox pointers
         cand = eligible_commits(prog, gpu_of)
         if not cand:
             return
@@ -233,6 +234,12 @@ class InboxSet:
     def by_task(self) -> dict:
         return {ib.commit.task.coord: ib for ib in self.inboxes.values()}
 
+    def pin(self):
+        self.pins += 1
+
+    def unpin(self):
+        self.pins = max(0, self.pins - 1)
+
     def free(self):
         for ib in self.inboxes.values():
             ib.free()
@@ -275,8 +282,12 @@ def inbox_set(prog, world, gpu_of) -> InboxSet:
     if not eligible_commits(prog, gpu_of):     # nothing to map: do not evict a useful set
         return _NO_INBOXES
     while len(reg) >= MAX_SETS:
-        old = reg.pop(next(iter(reg)))
-        old.release(world)
+        # the least recently created set nobody pins (a CUDA graph or launch plan
+        # holding its raw pointers keeps it alive; then the registry grows)
+        victim = next((k for k, v in reg.items() if not getattr(v, "pins", 0)), None)
+        if victim is None:
+            break
+        reg.pop(victim).release(world)
     s = InboxSet(prog, world, gpu_of)
     reg[id(prog)] = s
     return s

@@ -38,7 +38,7 @@ from .comm import world as current_world
 from .distribution import HyperRect, TensorDistribution, check_redistributable, subtract_rects
 from .errors import (ConfigError, ExtentMismatch, MissingDistribution, MissingInput, TendistError,
                      VerifyFail)
-from .interp import DeviceTile, execute_chain, stream_handle, torch_mod
+from .interp import DeviceTile, device_buffer, execute_chain, stream_handle, torch_mod
 from .ir import TensorIndexStmt, accesses_of
 from .leaves import BUILTIN_LEAVES, contracted_var, native_plan, run_leaf, run_native_box
 from .machine import Machine
@@ -490,6 +490,19 @@ def _leaf_choice(relations, loop_vars, policy):
     return policy, None
 
 
+class _NativeEvent:
+    """A plan-owned cudaEvent (td_event_create), usable where torch events are."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self, handle: int):
+        self.handle = handle
+
+
+def g_index(world, g) -> int:
+    return world.device(g).index
+
+
 class _Executor:
     def __init__(self, prog, store: RegionStore, policy: str):
         self.prog = prog
@@ -506,6 +519,7 @@ class _Executor:
         self.gpus = sorted({self.gpu(t.coord) for t in self.plan.tasks} |
                            {g for g in self.W.owned})
         self.owned = [g for g in self.gpus if self.W.owns(g)]
+        self.credits = {}            # id(inbox) -> plan-owned credit event (while recording)
 
     def gpu(self, p) -> int:
         return self.m.device_of(p, self.W.ngpus)
@@ -537,9 +551,30 @@ class _Executor:
             self.store.wait_ready(stream, o[0], o[1], o[2], rect)
 
     def _sync(self, waiter, producer):
-        ev = self.torch.cuda.Event()
-        ev.record(producer)
-        waiter.wait_event(ev)
+        self._after(waiter, self._mark(producer))
+
+    def _mark(self, stream):
+        """An event on `stream` at this point (a plan-owned native event and a
+        plan op while a launch plan is being recorded)."""
+        rec = _native.recorder()
+        if rec is None:
+            ev = self.torch.cuda.Event()
+            ev.record(stream)
+            return ev
+        h = rec.event(stream.device.index)
+        _native.call("td_event_record", C.c_void_p(h), stream_handle(stream))
+        return _NativeEvent(h)
+
+    @staticmethod
+    def _after(stream, ev, record=True):
+        """`stream` waits for `ev` (torch or native event)."""
+        if isinstance(ev, _NativeEvent):
+            if record:
+                _native.call("td_stream_wait_event", stream_handle(stream), C.c_void_p(ev.handle))
+            else:
+                _native.check(_native.lib().td_stream_wait_event(stream_handle(stream), C.c_void_p(ev.handle)))
+        else:
+            stream.wait_event(ev)
 
     # ---- phases
     def run(self):
@@ -562,12 +597,16 @@ class _Executor:
                 ib = self.inbox.get(t.coord)
                 if ib is not None:
                     if ib.credit is not None and not _CAPTURING:   # the home has released the inbox
-                        self.cstream(g).wait_event(ib.credit)
+                        self._after(self.cstream(g), ib.credit, record=False)
+                    rec = _native.recorder()
+                    if rec is not None:
+                        # a replay's leaf waits for the previous replay's release of the inbox
+                        h = self.credits[id(ib)] = rec.event(g_index(self.W, g))
+                        _native.call("td_stream_wait_event", stream_handle(self.cstream(g)), C.c_void_p(h))
                     self.out_bufs[t.coord] = ib.writer_view()
                     continue
-                with torch.cuda.stream(self.cstream(g)):
-                    self.out_bufs[t.coord] = torch.zeros(t.out_rect.shape, dtype=torch.float64,
-                                                         device=self.W.device(g))
+                self.out_bufs[t.coord] = device_buffer(t.out_rect.shape, self.W.device(g), self.cstream(g),
+                                                       zero=True)
         nsteps = self.plan.num_steps
         if self._local_only():
             self._run_task_major(out_region)
@@ -643,7 +682,10 @@ class _Executor:
             self._mark_done(region, mine, upto=task.coord)
 
     def _mark_done(self, region, commits, upto=None):
-        """Record, per output piece, an event after its last commit."""
+        """Record, per output piece, an event after its last commit (eager
+        runs only: replayed plans clear `store.done` for their output)."""
+        if _native.recorder() is not None:
+            return
         last = {}
         for c in self.prog.commits:
             last[(self.gpu(c.home), c.color)] = c.task.coord
@@ -718,17 +760,13 @@ class _Executor:
         view = _slice(self.holding_buf(t.src_hid), src_h.rect, part)
         if not view.is_contiguous():
             st = self.xstream(gs)
-            with torch.cuda.stream(st):
-                packed = torch.empty(part.shape, dtype=torch.float64, device=view.device)
+            packed = device_buffer(part.shape, view.device, st)
             _copy_box(st, packed, view)
             view = packed
         return view
 
     def _recv_buf(self, gd, part):
-        torch = self.torch
-        st = self.xstream(gd)
-        with torch.cuda.stream(st):
-            buf = torch.empty(part.shape, dtype=torch.float64, device=self.W.device(gd))
+        buf = device_buffer(part.shape, self.W.device(gd), self.xstream(gd))
         buf.record_stream(self.cstream(gd))
         return buf
 
@@ -811,8 +849,7 @@ class _Executor:
         if len(hids) == 1 and self.prog.holdings[hids[0]].rect.contains(rect):
             h = self.prog.holdings[hids[0]]
             return _slice(self.holding_buf(hids[0]), h.rect, rect)
-        with torch.cuda.stream(st):
-            buf = torch.zeros(rect.shape, dtype=torch.float64, device=self.W.device(g))
+        buf = device_buffer(rect.shape, self.W.device(g), st, zero=True)
         for hid in hids:
             h = self.prog.holdings[hid]
             part = h.rect.intersect(rect) if rect.lo else rect
@@ -916,8 +953,7 @@ class _Executor:
                 if self.W.owns(gd):
                     dst = _slice(full[t.dst_hid], t.part, sub)
                     if not dst.is_contiguous():
-                        with torch.cuda.stream(self.xstream(gd)):
-                            stage = torch.empty(sub.shape, dtype=torch.float64, device=self.W.device(gd))
+                        stage = device_buffer(sub.shape, self.W.device(gd), self.xstream(gd))
                         unpack.append((gd, dst, stage))
                         dst = stage
                     recvs.append((gd, gs, dst))
@@ -925,9 +961,7 @@ class _Executor:
             for gd, dst, stage in unpack:
                 _copy_box(self.xstream(gd), dst, stage)
             for g in self.owned:
-                ev = torch.cuda.Event()
-                ev.record(self.xstream(g))
-                events[g].append(ev)
+                events[g].append(self._mark(self.xstream(g)))
         return events
 
     def compute_split(self, works, s, split, events):
@@ -942,7 +976,7 @@ class _Executor:
             if not self.W.owns(g) or w.task.out_rect is None:
                 continue
             st = self.cstream(g)
-            st.wait_event(events[g][0])
+            self._after(st, events[g][0])
             acc = 0 if w.task.coord in self.inbox else 1
             if any(rect is None for _, rect, _ in w.operands.values()):
                 if not acc:   # an empty access: the partial is all zeros
@@ -976,14 +1010,14 @@ class _Executor:
         ins = [tiles[(a.tensor.name, a.var_names)] for a in rhs]
         for c, (a, b) in enumerate(_k_cuts(*box[kv], self.store.first_step_pieces)):
             if c and events:
-                st.wait_event(events[min(c, len(events) - 1)])
+                self._after(st, events[min(c, len(events) - 1)])
             for hid, rect, ax in lazy:
                 self.wait_piece(st, hid, _with_range(rect, ax, a, b))
             sub = dict(box)
             sub[kv] = (a, b)
             run_native_box(m, leaf, sub, out_tile, ins, st, acc if c == 0 else 1)
         for e in (events or [])[1:]:
-            st.wait_event(e)
+            self._after(st, e)
 
     def compute(self, works, s):
         plan = self.plan
@@ -1108,15 +1142,12 @@ class _Executor:
                 view = _slice(self.out_bufs[c.task.coord], c.task.out_rect, c.part)
                 if not view.is_contiguous():
                     st = self.xstream(gt)
-                    with torch.cuda.stream(st):
-                        packed = torch.empty(c.part.shape, dtype=torch.float64, device=view.device)
+                    packed = device_buffer(c.part.shape, view.device, st)
                     _copy_box(st, packed, view)
                     view = packed
                 sends.append((gt, gh, view))
             if self.W.owns(gh):
-                st = self.xstream(gh)
-                with torch.cuda.stream(st):
-                    buf = torch.empty(c.part.shape, dtype=torch.float64, device=self.W.device(gh))
+                buf = device_buffer(c.part.shape, self.W.device(gh), self.xstream(gh))
                 buf.record_stream(self.cstream(gh))
                 staged[k] = buf
                 recvs.append((gh, gt, buf))
@@ -1137,15 +1168,17 @@ class _Executor:
             self._nccl(sends, recvs)
             for ib, tw, th in tokens:
                 if tw is not None and not _CAPTURING:
-                    ev = self.torch.cuda.Event()
-                    ev.record(self.xstream(ib.writer_gpu))
-                    ib.credit = ev
+                    h = self.credits.get(id(ib))
+                    if h is not None:       # recording: the plan's own credit event
+                        _native.call("td_event_record", C.c_void_p(h), stream_handle(self.xstream(ib.writer_gpu)))
+                        ib.credit = _NativeEvent(h)
+                    else:
+                        ev = self.torch.cuda.Event()
+                        ev.record(self.xstream(ib.writer_gpu))
+                        ib.credit = ev
 
     def _token(self, g):
-        torch = self.torch
-        with torch.cuda.stream(self.xstream(g)):
-            t = torch.empty(1, dtype=torch.float64, device=self.W.device(g))
-        return t
+        return device_buffer((1,), self.W.device(g), self.xstream(g))
 
 
 _PLAN_CACHE: dict = {}
@@ -1195,7 +1228,7 @@ def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: 
     if trace is None:
         trace = ExecutionTrace(store.machine)
     prog = _plan_cached(stmt, store, trace, record_requirements)
-    _Executor(prog, store, leaf_policy).run()
+    _launch(prog, store, leaf_policy)
     plan = prog.plan
     out_region = store[plan.out_name]
     out_region.zeroed = False
@@ -1214,6 +1247,93 @@ def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: 
 
 
 _CAPTURING = False      # inside CapturedLaunch's capture: no cross-launch events
+
+# ---------------------------------------------------------------- launch plans
+# Repeated launches of one program on one store (benchmark steps, iterative
+# solvers) replay a recorded plan: the second execute of a (program, store
+# layout, streams) runs eagerly while `_native.recording` collects every
+# native call it issues -- leaves, box copies, fills, NCCL groups, event
+# edges -- with their device pointers; from the third on, `td_execute_plan`
+# issues that op array in one C++ call (csrc/plan.cu), so the per-step loop
+# no longer runs in Python.  Temporaries of the recorded run stay allocated
+# for the plan's lifetime.  Not recorded: Python leaf plugins, progressive
+# uploads / row streaming (e2e hooks that hand events to the caller), leaf
+# timing, CUDA-graph capture.
+PLANS = True
+PLAN_MAX_BYTES_PER_GPU = 24 << 30
+PLANS_PER_STORE = 8
+
+
+def _plannable(prog, store, policy) -> bool:
+    from . import leaves as _leaves
+    if not PLANS or _CAPTURING or _leaves.TIMING is not None or _native.recorder() is not None:
+        return False
+    if store.ready or store.pending or store.stream_rows >= 2:
+        return False
+    task_loops, _ = _loops_of(prog.plan.task_body)
+    _, plugins = _leaf_choice(prog.plan.relations, [v for v, _, _ in task_loops], policy)
+    return not plugins
+
+
+def _plan_key(prog, store, policy):
+    torch = torch_mod()
+    W = store.world
+    out = store[prog.plan.out_name]
+    pieces = tuple((n, tuple((k, b.data_ptr()) for k, b in r.pieces.items())) for n, r in store.regions.items())
+    streams = tuple(torch.cuda.current_stream(W.device(g)).cuda_stream for g in W.owned)
+    return (id(prog), policy, out.zeroed, pieces, streams)
+
+
+def _launch(prog, store, policy) -> None:
+    """Run one launch: eagerly, recording a plan, or replaying one."""
+    if not _plannable(prog, store, policy):
+        _Executor(prog, store, policy).run()
+        return
+    cache = store.__dict__.setdefault("_launch_plans", {})
+    key = _plan_key(prog, store, policy)
+    hit = cache.get(key)
+    if isinstance(hit, tuple) and hit[0] is prog:
+        _replay(hit[1], prog, store)
+        return
+    if hit != "seen":
+        if hit is None:
+            cache[key] = "seen"
+        _Executor(prog, store, policy).run()
+        return
+    with _native.recording() as rec:
+        ex = _Executor(prog, store, policy)
+        ex.run()
+    per_gpu = {}
+    for t in rec.keep:
+        if hasattr(t, "data_ptr") and t.is_cuda:
+            per_gpu[t.device.index] = per_gpu.get(t.device.index, 0) + t.numel() * 8
+    if not rec.valid or max(per_gpu.values(), default=0) > PLAN_MAX_BYTES_PER_GPU:
+        cache[key] = "never"
+        return
+    plan = rec.finish()
+    sets = [] if not ex.inbox else [peer.inbox_set(prog, store.world, ex.gpu)]
+    plan.extra["credits"] = [(ib, h) for ib in ex.inbox.values() for i, h in ex.credits.items() if i == id(ib)]
+    plan.extra["inbox_sets"] = sets
+    for st in sets:
+        st.pin()
+        weakref.finalize(plan, st.unpin)
+    while len(cache) >= PLANS_PER_STORE:
+        cache.pop(next(iter(cache)))
+    cache[key] = (prog, plan)
+
+
+def _replay(plan, prog, store) -> None:
+    W = store.world
+    for ib, h in plan.extra["credits"]:
+        # an eager launch in between left a torch credit event the plan does not know
+        if ib.credit is not None and not isinstance(ib.credit, _NativeEvent):
+            W.streams(ib.writer_gpu)[0].wait_event(ib.credit)
+    plan.run()
+    for ib, h in plan.extra["credits"]:
+        ib.credit = _NativeEvent(h)
+    out = prog.plan.out_name
+    store.done = {k: v for k, v in store.done.items() if k[0] != out}
+    store.row_done = {k: v for k, v in store.row_done.items() if k[0] != out}
 
 
 class CapturedLaunch:
@@ -1259,6 +1379,12 @@ class CapturedLaunch:
         finally:
             _CAPTURING = False
         self.trace = plan_trace
+        # the graph holds raw peer-inbox pointers: keep their InboxSet alive
+        # (not evicted by later programs) for the graph's lifetime
+        iset = W.inbox_sets.get(id(prog)) if hasattr(W, "inbox_sets") else None
+        if iset is not None and iset.prog is prog and getattr(iset, "inboxes", None):
+            iset.pin()
+            weakref.finalize(self, iset.unpin)
 
     def replay(self) -> None:
         self.graph.replay()
