@@ -135,6 +135,8 @@ class TdGemmProblem(C.Structure):
                 ("B", C.c_void_p), ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64)]
 
 
+_SIGNATURES["td_dgemm_grouped"] = ([vp, i32, C.POINTER(TdGemmProblem), i32], i32)
+
 _RECORDING = None
 
 

@@ -47,7 +47,8 @@ BUILTIN_LEAVES = frozenset({"auto", "dgemm", "gemm", "ttv", "ttm", "mttkrp", "in
 _ENUM_LIMIT = 1 << 22
 
 # counters for the bench / tests: which path each step took
-STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0}
+STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0, "grouped": 0,
+         "k_merged": 0}
 
 
 # optional per-launch device timing: set TIMING = [] to collect
@@ -232,13 +233,15 @@ def _launch_native(m: Match, leaf, box, out: DeviceTile, ins, stream, accumulate
     st = {r: t.strides() for r, t in v.items()}
     ost = o.strides()
     ext = {n: hi - lo for n, (lo, hi) in box.items()}
+    if m.kind != "dgemm":
+        flush_pending()
     if m.kind == "dgemm":
         a, b = leaf.lhs.var_names
         c = accs[m.roles["A"]].var_names[1]
         if st["A"][1] != 1 or st["B"][1] != 1 or ost[1] != 1:
             return False
-        _native.call("td_dgemm", s, ext[a], ext[b], ext[c], _p(v["A"]), st["A"][0], _p(v["B"]),
-                     st["B"][0], _p(o), ost[0], accumulate)
+        _dgemm(stream, ext[a], ext[b], ext[c], v["A"].ptr(), st["A"][0], v["B"].ptr(), st["B"][0], o.ptr(),
+               ost[0], accumulate, keep=(v["A"].data, v["B"].data, o.data))
     elif m.kind == "ttv":
         a, b = leaf.lhs.var_names
         c = accs[m.roles["c"]].var_names[0]
@@ -428,6 +431,112 @@ def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate
     return True
 
 
+# ------------------------------------------------------------ GEMM batches
+class gemm_batch:
+    """Context: plain GEMM leaves issued inside it are deferred and launched
+    at exit by `_flush_gemms` (k-continuations merged, then grouped launches
+    of <= 8 independent output tiles, td_dgemm_grouped).  The executor wraps
+    one step's leaves of the tasks co-located on a GPU in it, and the whole
+    step loop of a GPU-local program (nothing moves between its steps: every
+    transfer is an alias).  Merging a task's k-slab steps into one GEMM
+    reassociates its k sum: exact on integer data, within gamma_K otherwise
+    (the "exact" policy never reaches here).  Inactive while leaves are
+    timed (TIMING), since the timing events bracket single launches."""
+
+    def __enter__(self):
+        global _GEMM_BATCH
+        self.outer = _GEMM_BATCH
+        if self.outer is None and TIMING is None:
+            _GEMM_BATCH = []
+        return self
+
+    def __exit__(self, *exc):
+        global _GEMM_BATCH
+        if self.outer is None and _GEMM_BATCH is not None:
+            pending, _GEMM_BATCH = _GEMM_BATCH, None
+            if exc[0] is None:
+                _flush_gemms(pending)
+        return False
+
+
+_GEMM_BATCH = None
+
+
+def _dgemm(stream, M, N, K, a, lda, b, ldb, c, ldc, accumulate, keep=()) -> None:
+    """td_dgemm, or deferred into the active gemm_batch (holding `keep`, the
+    operand tensors, until the grouped launch is issued: temporaries such
+    as assembled operands must not return to the allocator before that)."""
+    if _GEMM_BATCH is not None and M > 0 and N > 0 and K > 0:
+        _GEMM_BATCH.append((stream, accumulate, (M, N, K, a, lda, b, ldb, c, ldc), keep))
+        return
+    _native.call("td_dgemm", stream_handle(stream), M, N, K, C.c_void_p(a), lda, C.c_void_p(b), ldb,
+                 C.c_void_p(c), ldc, accumulate)
+
+
+def _k_adjacent(first, nxt) -> bool:
+    """Does GEMM `nxt` continue `first` along k (same C, same operand
+    layouts, A and B advanced by exactly first's K)?"""
+    m, n, k, a, lda, b, ldb, c, ldc = first
+    return (nxt[0] == m and nxt[1] == n and nxt[7] == c and nxt[8] == ldc and nxt[4] == lda
+            and nxt[6] == ldb and nxt[3] == a + 8 * k and nxt[5] == b + 8 * k * ldb)
+
+
+def _flush_gemms(pending) -> None:
+    """Issue deferred GEMMs: per output tile, consecutive GEMMs continuing
+    each other along k (a task's steps reading k-slabs of the same resident
+    pieces) merge into one longer-k GEMM; then round r launches the r-th
+    GEMM of every output tile, grouped 8 per launch.  Output tiles are
+    independent, and each tile's GEMMs keep their order."""
+    by_stream = {}
+    for stream, acc, prob, _keep in pending:
+        by_stream.setdefault(id(stream), (stream, {}))[1].setdefault(prob[7], []).append([acc, prob])
+    for stream, per_c in by_stream.values():
+        for seq in per_c.values():
+            merged = [seq[0]]
+            for acc, prob in seq[1:]:
+                last = merged[-1]
+                if acc == 1 and _k_adjacent(last[1], prob):
+                    last[1] = last[1][:2] + (last[1][2] + prob[2],) + last[1][3:]
+                    STATS["k_merged"] += 1
+                else:
+                    merged.append([acc, prob])
+            seq[:] = merged
+        depth = max(len(seq) for seq in per_c.values())
+        for r in range(depth):
+            items = [seq[r] for seq in per_c.values() if r < len(seq)]
+            for acc in (0, 1):
+                probs = [p for a, p in items if a == acc]
+                for lo in range(0, len(probs), GROUP_MAX):
+                    _launch_group(stream, probs[lo:lo + GROUP_MAX], acc)
+    for stream, _acc, _prob, keep in pending:   # operands stay allocated until the launches ran
+        for t in keep:
+            if hasattr(t, "record_stream") and t.is_cuda:
+                t.record_stream(stream)
+
+
+def flush_pending() -> None:
+    """Issue the deferred GEMMs now (the batch stays open): called before any
+    write that is not deferred, so per-tile write order is kept."""
+    global _GEMM_BATCH
+    if _GEMM_BATCH:
+        pending, _GEMM_BATCH = _GEMM_BATCH, []
+        _flush_gemms(pending)
+
+
+def _launch_group(stream, chunk, acc) -> None:
+    if len(chunk) == 1:
+        m, n, k, a, lda, b, ldb, c, ldc = chunk[0]
+        _native.call("td_dgemm", stream_handle(stream), m, n, k, C.c_void_p(a), lda, C.c_void_p(b), ldb,
+                     C.c_void_p(c), ldc, acc)
+        return
+    arr = (_native.TdGemmProblem * len(chunk))(*[_native.TdGemmProblem(*p) for p in chunk])
+    _native.call("td_dgemm_grouped", stream_handle(stream), len(chunk), arr, acc)
+    STATS["grouped"] += 1
+
+
+GROUP_MAX = 8
+
+
 def _timing_start(stream):
     if TIMING is None:
         return None
@@ -508,6 +617,7 @@ def run_native_box(m, leaf, box, out: DeviceTile, ins, stream, accumulate: int =
 
 def _zero_tile(out: DeviceTile, stream) -> None:
     """out = +0.0 on `stream` (contiguous tiles, including peer inboxes)."""
+    flush_pending()
     data = out.data
     if not data.is_contiguous():
         raise TendistError(f"cannot zero the strided output tile {out!r}")
@@ -547,6 +657,7 @@ def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream, accum
         raise ConfigError(f"leaf kernel {policy!r} needs a reduction statement")
     if not zeroed:
         _zero_tile(out, stream)
+    flush_pending()
     run_nest(loops, leaf, defs, out, ins, stream)
     STATS["nest"] += 1
     return "nest"

@@ -40,7 +40,7 @@ from .errors import (ConfigError, ExtentMismatch, MissingDistribution, MissingIn
                      VerifyFail)
 from .interp import DeviceTile, device_buffer, execute_chain, stream_handle, torch_mod
 from .ir import TensorIndexStmt, accesses_of
-from .leaves import BUILTIN_LEAVES, contracted_var, native_plan, run_leaf, run_native_box
+from .leaves import BUILTIN_LEAVES, contracted_var, flush_pending, native_plan, run_leaf, run_native_box
 from .machine import Machine
 from .planner import build_program
 from .tensors import DenseTensor
@@ -490,6 +490,14 @@ def _leaf_choice(relations, loop_vars, policy):
     return policy, None
 
 
+class _NoBatch:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 class _NativeEvent:
     """A plan-owned cudaEvent (td_event_create), usable where torch events are."""
 
@@ -608,9 +616,31 @@ class _Executor:
                 self.out_bufs[t.coord] = device_buffer(t.out_rect.shape, self.W.device(g), self.cstream(g),
                                                        zero=True)
         nsteps = self.plan.num_steps
-        if self._local_only():
+        local = self._local_only()
+        if local and self._early_outputs():
             self._run_task_major(out_region)
         else:
+            from .leaves import gemm_batch
+            batch = gemm_batch() if local and not self._reads_output() else _NoBatch()
+            with batch:
+                self._steps(nsteps)
+            if not self.prog.stepwise:
+                self.compute(self.prog.work[-1], -1)
+            self.commit(out_region)
+            self._mark_done(out_region, self.prog.commits)
+        for g in self.owned:
+            cur = torch.cuda.current_stream(self.W.device(g))
+            self._sync(cur, self.cstream(g))
+            self._sync(cur, self.xstream(g))
+        self.buffers.clear()
+        self.out_bufs.clear()
+
+    def _reads_output(self) -> bool:
+        return self.plan.out_name in {a.tensor.name for leaf in leaf_statements(self.plan.task_body)
+                                      for a in accesses_of(leaf.rhs)}
+
+    def _steps(self, nsteps):
+        if True:
             for s in range(nsteps):
                 if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
                     for g in self.owned:
@@ -626,16 +656,6 @@ class _Executor:
                 if self.prog.stepwise:
                     self.compute(self.prog.work[s], s)
                 self.release(s)
-            if not self.prog.stepwise:
-                self.compute(self.prog.work[-1], -1)
-            self.commit(out_region)
-            self._mark_done(out_region, self.prog.commits)
-        for g in self.owned:
-            cur = torch.cuda.current_stream(self.W.device(g))
-            self._sync(cur, self.cstream(g))
-            self._sync(cur, self.xstream(g))
-        self.buffers.clear()
-        self.out_bufs.clear()
 
     def _inboxes(self) -> dict:
         """{task coord: peer.Inbox} of the write-backs that go through peer
@@ -657,6 +677,14 @@ class _Executor:
                 if self.gpu(t.src) != self.gpu(t.dst):
                     return False
         return all(self.gpu(c.task.coord) == self.gpu(c.home) for c in self.prog.commits)
+
+    def _early_outputs(self) -> bool:
+        """Does a caller consume output pieces as they finish (e2e: inputs
+        still uploading, rows streamed out)?  Then GPU-local programs run
+        task-major; otherwise step-major, where one step's leaves of all the
+        co-located tasks go out as grouped launches."""
+        st = self.store
+        return bool(st.ready or st.pending or st.stream_rows >= 2)
 
     def _run_task_major(self, region):
         """Task-major order for GPU-local programs: each task runs all its
@@ -1020,6 +1048,11 @@ class _Executor:
             self._after(st, e)
 
     def compute(self, works, s):
+        from .leaves import gemm_batch
+        with gemm_batch() if not self._early_outputs() else _NoBatch():
+            self._compute(works, s)
+
+    def _compute(self, works, s):
         plan = self.plan
         task_loops, leaf = _loops_of(plan.task_body)
         loop_vars = [v for v, _, _ in task_loops]
@@ -1059,6 +1092,7 @@ class _Executor:
                 continue
             if plugins:
                 read = {a.tensor.name: tiles[(a.tensor.name, a.var_names)] for a in rhs}
+                flush_pending()
                 execute_chain(loops[len(w.task.env):], leaf, dict(w.task.env), plan.defs, read,
                               {plan.out_name: out_tile}, plugins, st, self.W.device(g))
             else:

@@ -125,7 +125,7 @@ def test_grouped_gemm_equals_separate_launches():
         assert lib.td_dgemm(C.c_void_p(st), m, n, k, C.c_void_p(a.data_ptr()), k, C.c_void_p(b.data_ptr()), n,
                             C.c_void_p(c1.data_ptr()), n, 1) == 0
         sep.append((c0, c1))
-    assert lib.td_dgemm_grouped(C.c_void_p(st), len(shapes), C.addressof(probs), 1) == 0
+    assert lib.td_dgemm_grouped(C.c_void_p(st), len(shapes), probs, 1) == 0
     torch.cuda.synchronize()
     for c0, c1 in sep:
         assert torch.equal(c0, c1)
