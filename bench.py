@@ -119,7 +119,7 @@ def _num(x):
 
 # ------------------------------------------------------------------ helpers
 class Job:
-    def __init__(self, n_gpus):
+    def __init__(self, n_gpus, procs=0):
         import torch
         self.torch = torch
         self.size = int(os.environ.get("WORLD_SIZE", "1"))
@@ -137,6 +137,9 @@ class Job:
         self.world = td.configure_distributed() if self.size > 1 else td.comm.world()
         self.device = self.world.device(self.world.owned[0])
         self.n_gpus = max(n_gpus, self.size)
+        # logical processors of the BASELINE layout (default one per GPU; e.g. 8 on 4 GPUs
+        # runs the p = 8 programs two processors per GPU, Machine.device_of)
+        self.procs = procs or self.n_gpus
 
     def close(self):
         # same teardown order as tests/mp_check.py: communicators, then the process group
@@ -201,7 +204,7 @@ def _profile_traffic(name):
 def bench_gemm(job, steps, warmup, e2e_steps):
     td, torch = job.td, job.torch
     from paper_2203_08069_b200 import leaves, _native
-    p = job.n_gpus
+    p = job.procs
     n = td.weak_gemm_n(p)
     bundle = td.gemm_for_gpus(p, n)
     cin, store = bundle.prepare(seed=0, mode=0, world=job.world)
@@ -243,19 +246,20 @@ def bench_gemm(job, steps, warmup, e2e_steps):
     # roofline of the dominant kernel on this rank: the rank's algorithmic GEMM flop
     # over the summed device time of its DMMA launches (the pipelined first step
     # runs its k-range as two launches, so launches differ in size)
-    flop_per_launch = 2.0 * n ** 3 / p * steps / n_dgemm if n_dgemm else None
+    flop_per_launch = 2.0 * n ** 3 / job.n_gpus * steps / n_dgemm if n_dgemm else None
     achieved = flop_per_launch / (dgemm_ms / 1e3) / 1e12 if dgemm_ms else None
 
     # e2e through the public API with host buffers
     del store, step
     gc.collect()
     torch.cuda.empty_cache()
-    e2e = bench_gemm_e2e(job, bundle, cin, e2e_steps)
+    e2e = bench_gemm_e2e(job, bundle, cin, e2e_steps) if job.procs == job.n_gpus else {
+        "value": None, "unit": "GFLOP/s", "note": f"{job.procs} processors on {job.n_gpus} GPUs: device-resident only"}
     gc.collect()
     torch.cuda.empty_cache()
     return {
         "n": n, "bundle": bundle.name, "machine": str(bundle.machine), "ms_per_step": ms / steps,
-        "value": value, "per_gpu": value / p, "gpu_launches": launches, "launches_per_step": launches / steps,
+        "value": value, "per_gpu": value / job.n_gpus, "gpu_launches": launches, "launches_per_step": launches / steps,
         "dgemm_launches_timed": n_dgemm, "dgemm_ms_per_launch": dgemm_ms, "check": check,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
@@ -447,7 +451,7 @@ def _spot_check(job, bundle, store, per_piece=4):
 def bench_kernels(job, steps, warmup):
     td, torch = job.td, job.torch
     from paper_2203_08069_b200 import leaves
-    p = job.n_gpus
+    p = job.procs
     hbm = _peaks().get("hbm_gbs", 6544.3)
     results = {}
 
@@ -462,21 +466,25 @@ def bench_kernels(job, steps, warmup):
         for _ in range(warmup):
             step()
         # short steps (2-20 ms): time enough of them (>= ~100 ms) that the host's issue
-        # latency before the first step does not count against the device rate
+        # latency before the first step does not count against the device rate.  The
+        # step rate is measured with launch plans replaying (runtime._launch); the kernel
+        # rate in a second pass with per-leaf CUDA events (which runs the eager loop)
         est = job.timed(step, 1, 0)
         nsteps = max(steps, min(50, int(100.0 / max(est, 1e-3)) + 1))
-        leaves.TIMING = []
         ms = job.timed(step, nsteps, 0)
+        leaves.TIMING = []
+        ms_eager = job.timed(step, nsteps, 0)
         kms, nk = _leaf_timing(td, kind)
         leaves.TIMING = None
         check = _spot_check(job, bundle, store)
-        per_gpu_work = work / p
+        per_task_work = work / p          # one leaf launch per task per step
         rate = work * nsteps / (ms / 1e3) / 1e9
-        kern = per_gpu_work / (kms / 1e3) / 1e9 if kms else None
+        kern = per_task_work / (kms / 1e3) / 1e9 if kms else None
         results[name] = {
             "config": bundle.name + " " + str(bundle.machine) + " dims " + str(
                 tuple(bundle.statement.extents[v] for v in bundle.statement.var_order)),
-            "value": rate, "unit": unit, "per_gpu": rate / p, "ms_per_step": ms / nsteps, "steps": nsteps,
+            "value": rate, "unit": unit, "per_gpu": rate / job.n_gpus, "ms_per_step": ms / nsteps, "steps": nsteps,
+            "ms_per_step_eager_timed": ms_eager / nsteps,
             "kernel": kind, "kernel_ms": kms, "kernel_rate_per_gpu": kern,
             "frac_of_roof": (kern / roof) if kern else None, "roof": roof, "check": check,
         }
@@ -486,7 +494,8 @@ def bench_kernels(job, steps, warmup):
 
     n = 2048
     run("ttv_2048", td.ttv(p, dims=(n * p, n, n)), 8.0 * (n ** 3 + n + n * n) * p, "GB/s", hbm, "ttv")
-    run("innerprod3_2048", td.innerprod3(p, dims=(n * p, n, n)), 16.0 * n ** 3 * p, "GB/s", hbm, "innerprod")
+    if p <= job.n_gpus:     # 2 x 2048^3 per processor: two processors per GPU would exceed HBM
+        run("innerprod3_2048", td.innerprod3(p, dims=(n * p, n, n)), 16.0 * n ** 3 * p, "GB/s", hbm, "innerprod")
     g1, g2 = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}[p]
     m = 1024
     run("ttm_1024_64", td.ttm2d(g1, g2, dims=(m * g1, m * g2, m, 64)), 2.0 * m ** 3 * 64 * p, "GFLOP/s",
@@ -504,10 +513,17 @@ def bench_kernels(job, steps, warmup):
         store.zero("C")
         td.execute(cin, store, record_requirements=False)
 
-    ms = job.timed(g1_step, 20, 5)
+    from paper_2203_08069_b200 import runtime as rt
+    ms = job.timed(g1_step, 50, 5)               # launch plans replaying (td_execute_plan)
+    rt.PLANS = False
+    try:
+        ms_eager = job.timed(g1_step, 20, 3)     # the Python step loop every time
+    finally:
+        rt.PLANS = True
     results["summa_1024_2x2"] = {"config": "summa 2x2 dims (1024, 1024, 1024) chunk 128", "value":
-                                 2.0 * 1024 ** 3 * 20 / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
-                                 "ms_per_step": ms / 20, "scaling": "strong (fixed size)"}
+                                 2.0 * 1024 ** 3 * 50 / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
+                                 "ms_per_step": ms / 50, "ms_per_step_python_loop": ms_eager / 20,
+                                 "check": _spot_check(job, g1, store), "scaling": "strong (fixed size)"}
     if job.world.ngpus == 1 or job.world.nprocs == job.world.ngpus:   # captured once as a CUDA graph, replayed
         from paper_2203_08069_b200.runtime import CapturedLaunch
         cap = CapturedLaunch(cin, store)
@@ -644,11 +660,13 @@ def main():
     ap.add_argument("--workload", default="all", choices=["all", "gemm"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--procs", type=int, default=0,
+                    help="logical processors of the BASELINE layout (default: one per GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
         return
-    job = Job(args.gpus)
+    job = Job(args.gpus, args.procs)
     gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps)
     kernels = bench_kernels(job, max(2, args.steps // 2), max(3, args.warmup)) if args.workload == "all" else None
     if job.rank == 0:
@@ -656,12 +674,14 @@ def main():
     job.close()
 
 
-def gemm_config(td, p):
+def gemm_config(td, p, gpus=None):
     """The headline workload's `config` -- identical in both arms."""
     n = td.weak_gemm_n(p)
     b = td.gemm_for_gpus(p, n)
+    gpus = gpus or p
+    par = f"{p} GPU(s), one task per GPU" if gpus == p else f"{p} processors on {gpus} GPUs"
     return {"workload": f"fp64 GEMM {n}^3 weak-scaled from 16384^3 ({b.name} on {b.machine})", "n": n,
-            "algorithm": b.name, "grid": str(b.machine), "parallelism": f"{p} GPU(s), one task per GPU",
+            "algorithm": b.name, "grid": str(b.machine), "parallelism": par,
             "l2": "inputs (>= 2 GiB per operand) exceed the 126 MB L2; no flush needed",
             "inputs": "integer-valued fp64 in [-4,4]"}
 
@@ -682,7 +702,7 @@ def report(args, job, gemm, kernels):
         "metric": METRIC, "value": gemm["value"], "unit": "GFLOP/s", "n_gpus": p, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": gemm["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": gemm_config(job.td, p),
+        "config": gemm_config(job.td, job.procs, job.n_gpus),
         "per_gpu": gemm["per_gpu"], "check": gemm["check"], "roofline": gemm["roofline"],
         "cpu_baseline": cpu, "e2e": gemm["e2e"], "gpu_launches": gemm["gpu_launches"],
         "gpu_launches_per_step": gemm["launches_per_step"], "clocks": gemm["clocks"],

@@ -65,8 +65,39 @@ def main():
         if not np.array_equal(res.output.data, np.asarray(want)):
             failures.append(f"oracle {b.name} {b.machine}")
 
-    # pipelined first step (k-pieces on the transfers and the GEMM leaves), forced on at test sizes
+    # 8 logical processors on the job's GPUs (two per GPU at 4 GPUs, Machine.device_of): the
+    # BASELINE p = 8 layouts -- Johnson 2x2x2, MTTKRP / TTM on 4x2, TTV / innerprod on 8
+    for b in (td.johnson(2, 2, 2, dims=(256, 192, 320)), td.mttkrp(4, 2, dims=(64, 24, 48, 40)),
+              td.ttm2d(4, 2, dims=(32, 24, 40, 16)), td.ttv(8, dims=(40, 12, 90)),
+              td.innerprod3(8, dims=(48, 10, 70))):
+        res, ins = b.run(seed=4)
+        want = seq_eval(td.format_statement(b.statement), b.statement.extents,
+                        {n: t.data for n, t in ins.items()})
+        if not np.array_equal(res.output.data, np.asarray(want)):
+            failures.append(f"8-proc {b.name} {b.machine}")
+
+    # launch plans under SPMD: each rank records its own ops (NCCL groups, peer-inbox tokens and
+    # credits, leaves) on the second execute and replays them from the third
     from paper_2203_08069_b200 import runtime as rt
+    pcases = [td.summa(2, 1, dims=(200, 160, 512), chunk=64), td.cosma_like((1, 1, 2), (1, 1, 1), dims=(136, 120, 300)),
+              td.mttkrp(2, 1, dims=(48, 16, 40, 36)), td.johnson(2, 2, 2, dims=(96, 80, 112))]
+    if size >= 4:
+        pcases += [td.cannon(2, 2, dims=(200, 144, 176)), td.cosma_like((2, 1, 2), (1, 1, 1), dims=(130, 96, 150)),
+                   td.mttkrp(2, 2, dims=(40, 32, 48, 36))]
+    for b in pcases:
+        cin, store = b.prepare(seed=16, mode=0, world=world)
+        out = b.statement.lhs.tensor.name
+        ins = {n: generate(b.statement.tensors()[n].dims, 16, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+        for rep in range(5):
+            store.zero(out)
+            td.execute(cin, store)
+            if not np.array_equal(store[out].tensor.data, want):
+                failures.append(f"plan {b.name} {b.machine} run {rep}")
+        if not any(isinstance(v, tuple) for v in store.__dict__.get("_launch_plans", {}).values()):
+            failures.append(f"plan {b.name} {b.machine}: nothing recorded")
+
+    # pipelined first step (k-pieces on the transfers and the GEMM leaves), forced on at test sizes
     saved = rt.SPLIT_MIN_BYTES
     rt.SPLIT_MIN_BYTES = 0
     for b in (td.cannon(2, 2, dims=(520, 392, 1000)), td.johnson(2, 2, 2, dims=(264, 200, 1040)),
