@@ -235,11 +235,12 @@ typedef struct td_op {
 int td_execute_plan(const td_op* ops, int64_t count);
 
 /* Cross-stream edges of a plan (no timing): record on the producer stream,
- * wait on the consumer stream. */
+ * wait on the consumer stream.  `device` is the stream's device (a NULL
+ * stream is that device's legacy default stream). */
 int td_event_create(int device, void** event);
 int td_event_destroy(void* event);
-int td_event_record(void* event, void* stream);
-int td_stream_wait_event(void* stream, void* event);
+int td_event_record(void* event, void* stream, int device);
+int td_stream_wait_event(void* stream, void* event, int device);
 
 #ifdef __cplusplus
 }

@@ -68,8 +68,8 @@ _SIGNATURES = {
     "td_dgemm_grouped": ([vp, i32, vp, i32], i32),
     "td_event_create": ([i32, C.POINTER(vp)], i32),
     "td_event_destroy": ([vp], i32),
-    "td_event_record": ([vp, vp], i32),
-    "td_stream_wait_event": ([vp, vp], i32),
+    "td_event_record": ([vp, vp, i32], i32),
+    "td_stream_wait_event": ([vp, vp, i32], i32),
     "td_execute_plan": ([vp, i64], i32),
 }
 

@@ -33,14 +33,29 @@ int td_event_destroy(void* event) {
   return TD_OK;
 }
 
-int td_event_record(void* event, void* stream) {
-  td::StreamDevice sd(stream);
+// `device` owns the event and the stream (it also names the device whose
+// legacy default stream a NULL `stream` means).
+namespace {
+struct OnDevice {
+  int prev = -1;
+  explicit OnDevice(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~OnDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+int td_event_record(void* event, void* stream, int device) {
+  OnDevice on(device);
   TD_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), td::as_stream(stream)));
   return TD_OK;
 }
 
-int td_stream_wait_event(void* stream, void* event) {
-  td::StreamDevice sd(stream);
+int td_stream_wait_event(void* stream, void* event, int device) {
+  OnDevice on(device);
   TD_CUDA(cudaStreamWaitEvent(td::as_stream(stream), reinterpret_cast<cudaEvent_t>(event), 0));
   return TD_OK;
 }
@@ -107,9 +122,9 @@ int run_op(const td_op& o) {
       return td_reduce_sum(P<void*>(a[0]), P<void*>(a[1]), P<const double*>(a[2]), P<double*>(a[3]), a[4],
                            I(a[5]));
     case TD_OP_EVENT_RECORD:
-      return td_event_record(P<void*>(a[0]), P<void*>(a[1]));
+      return td_event_record(P<void*>(a[0]), P<void*>(a[1]), I(a[2]));
     case TD_OP_STREAM_WAIT:
-      return td_stream_wait_event(P<void*>(a[0]), P<void*>(a[1]));
+      return td_stream_wait_event(P<void*>(a[0]), P<void*>(a[1]), I(a[2]));
     default:
       td::set_error("unknown op kind %d", o.kind);
       return TD_ERR_ARG;

@@ -510,7 +510,7 @@ def _flush_gemms(pending) -> None:
                     _launch_group(stream, probs[lo:lo + GROUP_MAX], acc)
     for stream, _acc, _prob, keep in pending:   # operands stay allocated until the launches ran
         for t in keep:
-            if hasattr(t, "record_stream") and t.is_cuda:
+            if getattr(t, "is_cuda", False):
                 t.record_stream(stream)
 
 

@@ -569,18 +569,21 @@ class _Executor:
             ev = self.torch.cuda.Event()
             ev.record(stream)
             return ev
-        h = rec.event(stream.device.index)
-        _native.call("td_event_record", C.c_void_p(h), stream_handle(stream))
+        dev = stream.device.index
+        h = rec.event(dev)
+        _native.call("td_event_record", C.c_void_p(h), stream_handle(stream), dev)
         return _NativeEvent(h)
 
     @staticmethod
     def _after(stream, ev, record=True):
         """`stream` waits for `ev` (torch or native event)."""
         if isinstance(ev, _NativeEvent):
+            dev = stream.device.index
             if record:
-                _native.call("td_stream_wait_event", stream_handle(stream), C.c_void_p(ev.handle))
+                _native.call("td_stream_wait_event", stream_handle(stream), C.c_void_p(ev.handle), dev)
             else:
-                _native.check(_native.lib().td_stream_wait_event(stream_handle(stream), C.c_void_p(ev.handle)))
+                _native.check(_native.lib().td_stream_wait_event(stream_handle(stream), C.c_void_p(ev.handle),
+                                                                 dev))
         else:
             stream.wait_event(ev)
 
@@ -610,7 +613,8 @@ class _Executor:
                     if rec is not None:
                         # a replay's leaf waits for the previous replay's release of the inbox
                         h = self.credits[id(ib)] = rec.event(g_index(self.W, g))
-                        _native.call("td_stream_wait_event", stream_handle(self.cstream(g)), C.c_void_p(h))
+                        _native.call("td_stream_wait_event", stream_handle(self.cstream(g)), C.c_void_p(h),
+                                     g_index(self.W, g))
                     self.out_bufs[t.coord] = ib.writer_view()
                     continue
                 self.out_bufs[t.coord] = device_buffer(t.out_rect.shape, self.W.device(g), self.cstream(g),
@@ -1204,7 +1208,8 @@ class _Executor:
                 if tw is not None and not _CAPTURING:
                     h = self.credits.get(id(ib))
                     if h is not None:       # recording: the plan's own credit event
-                        _native.call("td_event_record", C.c_void_p(h), stream_handle(self.xstream(ib.writer_gpu)))
+                        _native.call("td_event_record", C.c_void_p(h), stream_handle(self.xstream(ib.writer_gpu)),
+                                     g_index(self.W, ib.writer_gpu))
                         ib.credit = _NativeEvent(h)
                     else:
                         ev = self.torch.cuda.Event()
