@@ -473,6 +473,17 @@ int dgemm_rowsum_tile_rows(int config) {
   }
 }
 
+bool dgemm_rowsum_fusable(int config, int64_t batch, const GemmArgs& a) {
+  switch (config) {
+#define TD_ROWSUM_TMA_ID(id, BM, BN, BK, WM, WN, ST, MINB) case id:
+    TD_GEMM_TMA_CONFIGS(TD_ROWSUM_TMA_ID)
+#undef TD_ROWSUM_TMA_ID
+      return tma_ok(std::min<int64_t>(batch, 2), a);
+    default:
+      return false;
+  }
+}
+
 int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
   const bool vec2 = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                     (batch == 1 || a.sA % 2 == 0);
@@ -481,6 +492,10 @@ int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a) {
     GemmArgs c = a;
     c.A += done * a.sA;
     c.C += done * a.sC;
+    if (c.counters) {
+      c.counters += done * a.N;
+      c.out += done * a.ldo;
+    }
     int rc = TD_ERR_ARG;
     switch (config) {
 #define TD_ROWSUM_CASE(id, BM, BN, BK, WM, WN, ST)                                              \

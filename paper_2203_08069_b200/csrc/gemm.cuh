@@ -22,10 +22,18 @@ struct GemmArgs {
   // of H(r, n) * (A.B)(r, n) -- one partial per M-tile, C is the workspace
   const double* H;
   int64_t ldh;
+  // EPI = 1, TMA body, fused finish: per-(batch, N-tile) arrival counters (zero
+  // between launches) and the output rows out + batch * ldo (+= if out_acc)
+  int* counters;
+  double* out;
+  int64_t ldo;
+  int out_acc;
 };
 
 // MTTKRP row-sum GEMMs (EPI = 1 in gemm.cu): rows per M-tile of a config, launch
 int dgemm_rowsum_tile_rows(int config);
 int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a);
+// Does `config` take the TMA body (whose epilogue can finish the sum itself)?
+bool dgemm_rowsum_fusable(int config, int64_t batch, const GemmArgs& a);
 
 }  // namespace td

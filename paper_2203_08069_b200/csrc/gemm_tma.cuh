@@ -189,6 +189,28 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
       for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
       if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
     }
+    if (p.counters != nullptr) {
+      // fused finish (replaces mttkrp_reduce): the last CTA of this (batch, N-tile)
+      // to arrive sums the M-tile partials in ascending order -- the same order,
+      // so the same bits -- and writes the output row
+      __shared__ int last_arrival;
+      __threadfence();
+      __syncthreads();
+      int* counter = p.counters + int64_t(bz) * p.N + tn;
+      if (tid == 0) last_arrival = atomicAdd(counter, 1) == p.tiles_m - 1;
+      __syncthreads();
+      if (last_arrival) {
+        __threadfence();
+        for (int c = tid; c < BN; c += Cfg::THREADS) {
+          if (n0 + c >= N) continue;
+          double v = 0.0;
+          for (int g = 0; g < p.tiles_m; ++g) v += __ldcg(C + int64_t(g) * N + n0 + c);
+          double* dst = p.out + int64_t(bz) * p.ldo + n0 + c;
+          *dst = p.out_acc ? *dst + v : v;
+        }
+        if (tid == 0) *counter = 0;  // ready for the next launch on this workspace
+      }
+    }
     return;
   }
 

@@ -26,6 +26,11 @@
 // fixed-order sum over the tile's k rows into the same [I][groups][R]
 // workspace; mttkrp_reduce finishes.  Measured 34.8 (TMA-fed body) and 33.4
 // (LDGSTS body) vs 30.9 TFLOP/s for the best fused configuration.
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "dmma.cuh"
 #include "gemm.cuh"
@@ -305,13 +310,54 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
 // MTTKRP as a batched GEMM over i whose epilogue does the Hadamard with C and
 // the sum over the k rows of each tile (gemm.cu, EPI = 1): the tile loop is
 // the tuned GEMM body, so B streams at the GEMM's rate.
+// Workspace of the GEMM-body MTTKRP, cached per (device, stream): the
+// [I][groups][R] partials and the per-(i, N-tile) arrival counters of the
+// fused finish (zeroed once; the last CTA of each row resets its counter).
+// One stream's launches are ordered, so they can share it; growth happens on
+// the first (largest) launch, outside any CUDA-graph capture.
+struct MkScratch {
+  double* work = nullptr;
+  size_t work_bytes = 0;
+  int* counters = nullptr;
+  size_t counter_bytes = 0;
+};
+
+static int mk_scratch(cudaStream_t st, size_t work_bytes, size_t counter_bytes, double** work, int** counters) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, MkScratch> cache;
+  int dev = 0;
+  TD_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  MkScratch& s = cache[{dev, st}];
+  if (s.work_bytes < work_bytes || s.counter_bytes < counter_bytes) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    TD_CUDA(cudaStreamIsCapturing(st, &cap));
+    TD_REQUIRE(cap == cudaStreamCaptureStatusNone,
+               "mttkrp: workspace must grow during CUDA-graph capture (run the launch once before capturing)");
+    TD_CUDA(cudaStreamSynchronize(st));
+    if (s.work) TD_CUDA(cudaFree(s.work));
+    if (s.counters) TD_CUDA(cudaFree(s.counters));
+    s.work_bytes = std::max(work_bytes, s.work_bytes);
+    s.counter_bytes = std::max(counter_bytes, s.counter_bytes);
+    TD_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.work), s.work_bytes));
+    TD_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.counters), s.counter_bytes));
+    TD_CUDA(cudaMemsetAsync(s.counters, 0, s.counter_bytes, st));
+  }
+  *work = s.work;
+  *counters = s.counters;
+  return TD_OK;
+}
+
 static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
   const int bm = dgemm_rowsum_tile_rows(gemm_config);
   TD_REQUIRE(bm > 0, "mttkrp: unknown GEMM row-sum config %d", gemm_config);
   a.groups = (int)std::max<int64_t>(1, ceil_div(a.K, bm));
-  if (int rc = retain_pool()) return rc;
-  TD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.work), sizeof(double) * a.I * a.groups * a.R, st));
+  int* counters = nullptr;
+  if (int rc = mk_scratch(st, sizeof(double) * std::max<int64_t>(1, a.I * a.groups * a.R),
+                          sizeof(int) * std::max<int64_t>(1, a.I * a.R), &a.work, &counters))
+    return rc;
   int rc = TD_OK;
+  bool fused = false;
   if (a.K > 0 && a.L > 0) {
     GemmArgs g{};
     g.M = a.K; g.N = a.R; g.K = a.L;
@@ -319,17 +365,21 @@ static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
     g.B = a.D; g.ldb = a.ldd; g.sB = 0;
     g.C = a.work; g.ldc = a.R; g.sC = int64_t(a.groups) * a.R;
     g.H = a.C; g.ldh = a.ldc;
+    fused = dgemm_rowsum_fusable(gemm_config, a.I, g);
+    if (fused) {  // the last CTA of every (i, N-tile) finishes the sum and writes A
+      g.counters = counters;
+      g.out = a.A; g.ldo = a.lda; g.out_acc = a.accumulate;
+    }
     rc = dgemm_rowsum(st, gemm_config, a.I, g);
   } else {
     TD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(double) * a.I * a.groups * a.R, st));
   }
-  if (rc == TD_OK) {
+  if (rc == TD_OK && !fused) {
     const int64_t outs = a.I * a.R;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(outs, 256), 148 * 8));
     mttkrp_reduce<<<blocks, 256, 0, st>>>(a.work, a.groups, a.I, a.R, a.A, a.lda, a.accumulate);
     rc = check_launch("mttkrp_reduce");
   }
-  TD_CUDA(cudaFreeAsync(a.work, st));
   return rc;
 }
 
