@@ -6,8 +6,10 @@ PKG       := paper_2203_08069_b200
 CSRC      := $(PKG)/csrc
 NCCL_ROOT ?= $(shell $(PY) -c "import nvidia.nccl,os;print(os.path.dirname(nvidia.nccl.__file__) if getattr(nvidia.nccl,'__file__',None) else list(nvidia.nccl.__path__)[0])")
 ARCH      := -gencode arch=compute_100a,code=sm_100a
+# TUNING=1 also builds the tile configurations kept only for td_dgemm_config sweeps
+TUNING    ?= 0
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr \
-             -I$(NCCL_ROOT)/include -Iinclude
+             -I$(NCCL_ROOT)/include -Iinclude $(if $(filter 1,$(TUNING)),-DTD_TUNING)
 LDFLAGS   := -shared -L$(NCCL_ROOT)/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_ROOT)/lib -cudart static
 SRCS      := $(CSRC)/capi.cu $(CSRC)/gemm.cu $(CSRC)/mttkrp.cu $(CSRC)/stream.cu $(CSRC)/interp.cu $(CSRC)/comm.cu $(CSRC)/peer.cu $(CSRC)/plan.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))

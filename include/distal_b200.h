@@ -187,6 +187,12 @@ int td_recv(void* comm, void* stream, double* buf, int64_t count, int peer);
 int td_bcast(void* comm, void* stream, double* buf, int64_t count, int root);
 int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count, int root);
 int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count);
+/* Host-side wait with a watchdog: returns when every stream is idle; while
+ * waiting polls ncclCommGetAsyncError on every communicator, and on an async
+ * error or after timeout_s seconds (<= 0: never) aborts ALL of them
+ * (ncclCommAbort, so stuck NCCL kernels return) and fails with TD_ERR_NCCL
+ * instead of hanging. */
+int td_comm_wait(void* const* comms, int ncomms, void* const* streams, int nstreams, double timeout_s);
 
 /* ---- peer memory over NVLink (csrc/peer.cu) ------------------------------
  * Reduce write-backs of the commit phase (reference simulator.py:624-654,

@@ -71,6 +71,7 @@ _SIGNATURES = {
     "td_event_record": ([vp, vp, i32], i32),
     "td_stream_wait_event": ([vp, vp, i32], i32),
     "td_execute_plan": ([vp, i64], i32),
+    "td_comm_wait": ([C.POINTER(vp), i32, C.POINTER(vp), i32, C.c_double], i32),
 }
 
 EXPORTED = tuple(_SIGNATURES)

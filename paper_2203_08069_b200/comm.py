@@ -22,7 +22,10 @@ import ctypes as C
 import os
 
 from . import _native
-from .errors import ConfigError, DeviceUnavailable
+from .errors import CommError, ConfigError, DeviceUnavailable
+
+#: seconds World.wait lets the GPUs go without progress before aborting NCCL
+NCCL_TIMEOUT_S = float(os.environ.get("TD_NCCL_TIMEOUT", "600"))
 
 
 class World:
@@ -110,9 +113,41 @@ class World:
             self._groups[key] = out
         return self._groups[key]
 
+    def all_comms(self) -> list:
+        return list(self.comms.values()) + [h for grp in self._groups.values() for h in grp.values()]
+
+    def wait(self, timeout: float = None) -> None:
+        """Block until this process's GPUs finished the launches issued so far,
+        with a watchdog instead of an unbounded sync: NCCL async errors are
+        polled while waiting, and on one -- or after `timeout` seconds without
+        completion (default TD_NCCL_TIMEOUT, 600 s) -- every communicator is
+        aborted (ncclCommAbort) and CommError is raised (td_comm_wait)."""
+        import torch
+        streams = []
+        for g in self.owned:
+            streams += [s.cuda_stream for s in self.streams(g)]
+            cur = torch.cuda.current_stream(self.device(g)).cuda_stream
+            if cur:
+                streams.append(cur)
+        comms = self.all_comms()
+        ca = (C.c_void_p * max(1, len(comms)))(*comms)
+        sa = (C.c_void_p * max(1, len(streams)))(*streams)
+        t = NCCL_TIMEOUT_S if timeout is None else float(timeout)
+        rc = _native.lib().td_comm_wait(ca, len(comms), sa, len(streams), t)
+        if rc < 0:
+            msg = _native.lib().td_last_error().decode(errors="replace")
+            self.comms, self._groups = {}, {}     # aborted: never destroy them again
+            self.broken = True
+            raise CommError(msg)
+        for g in self.owned:                      # the legacy default streams too
+            torch.cuda.synchronize(self.device(g))
+
     def close(self):
-        for s in self.inbox_sets.values():
-            s.release(self)        # after a device sync: no leaf still writes an inbox
+        if getattr(self, "broken", False):
+            self.inbox_sets = {}
+            return
+        from .peer import release_sets
+        release_sets(list(self.inbox_sets.values()), self)
         self.inbox_sets = {}
         for grp in self._groups.values():
             for h in grp.values():

@@ -8,7 +8,9 @@
 // process holds a single libnccl.
 #include "common.cuh"
 #include <nccl.h>
+#include <chrono>
 #include <cstring>
+#include <thread>
 
 #define TD_NCCL(call)                                                          \
   do {                                                                         \
@@ -100,6 +102,47 @@ int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, in
   TD_NCCL(ncclReduce(send, recv, (size_t)count, ncclDouble, ncclSum, root, static_cast<ncclComm_t>(comm),
                      td::as_stream(stream)));
   return TD_OK;
+}
+
+int td_comm_wait(void* const* comms, int ncomms, void* const* streams, int nstreams, double timeout_s) {
+  TD_REQUIRE((ncomms == 0 || comms) && (nstreams == 0 || streams), "comm_wait: null arrays");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    bool done = true;
+    for (int k = 0; k < nstreams; ++k) {
+      const cudaError_t e = cudaStreamQuery(td::as_stream(streams[k]));
+      if (e == cudaErrorNotReady) {
+        done = false;
+      } else if (e != cudaSuccess) {
+        td::set_error("comm_wait: stream %d failed: %s", k, cudaGetErrorString(e));
+        return TD_ERR_CUDA;
+      }
+    }
+    if (done) return TD_OK;
+    const char* why = nullptr;
+    char buf[256];
+    for (int k = 0; k < ncomms && !why; ++k) {
+      ncclResult_t ar = ncclSuccess;
+      if (ncclCommGetAsyncError(static_cast<ncclComm_t>(comms[k]), &ar) != ncclSuccess ||
+          (ar != ncclSuccess && ar != ncclInProgress)) {
+        std::snprintf(buf, sizeof buf, "NCCL communicator %d reported %s", k, ncclGetErrorString(ar));
+        why = buf;
+      }
+    }
+    const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (!why && timeout_s > 0 && waited > timeout_s) {
+      std::snprintf(buf, sizeof buf, "no progress after %.1f s (a peer never posted its side of a transfer?)",
+                    waited);
+      why = buf;
+    }
+    if (why) {
+      // abort every communicator: pending NCCL kernels return, the job can shut down
+      for (int k = 0; k < ncomms; ++k) ncclCommAbort(static_cast<ncclComm_t>(comms[k]));
+      td::set_error("comm_wait: %s; communicators aborted", why);
+      return TD_ERR_NCCL;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count) {

@@ -138,15 +138,28 @@ class Inbox:
     def writer_view(self):
         return RawView(self.writer_ptr, self.shape, device=self.writer_dev)
 
-    def free(self):
+    def close_mapping(self):
+        """Writer side: unmap another process's inbox (phase 1 of a release)."""
         try:
             if self.writer_ptr and self.opened:
                 _native.call("td_peer_close", self.writer_dev.index, C.c_void_p(self.writer_ptr))
+        except Exception:
+            pass
+        if self.opened:
+            self.writer_ptr = None
+
+    def free_home(self):
+        """Home side: free the allocation (phase 2, after every writer unmapped it)."""
+        try:
             if self.home_ptr:
                 _native.call("td_peer_free", self.home_dev.index, C.c_void_p(self.home_ptr))
         except Exception:
             pass
         self.home_ptr = self.writer_ptr = None
+
+    def free(self):
+        self.close_mapping()
+        self.free_home()
 
 
 class InboxSet:
@@ -246,14 +259,30 @@ class InboxSet:
         self.inboxes = {}
 
     def release(self, world):
-        """Free after the owned GPUs drained: no leaf still writes an inbox
-        (writer side) and every token was received (home side)."""
-        if not self.inboxes:
-            return
-        import torch
-        for g in world.owned:
-            torch.cuda.synchronize(world.device(g))
-        self.free()
+        """Free after the owned GPUs drained (no leaf still writes an inbox,
+        every token was received).  Collective in SPMD jobs, in two phases:
+        every writer unmaps its IPC mappings, all ranks meet, and only then
+        do the homes free the memory (freeing an exported allocation while
+        another process still maps it is undefined)."""
+        release_sets([self], world)
+
+
+def release_sets(sets, world) -> None:
+    """Two-phase release of several InboxSets (see InboxSet.release)."""
+    sets = [s for s in sets if getattr(s, "inboxes", None)]
+    if world.nprocs == 1 and not sets:
+        return
+    import torch
+    for g in world.owned:
+        torch.cuda.synchronize(world.device(g))
+    for st in sets:
+        for ib in st.inboxes.values():
+            ib.close_mapping()
+    world.all_gather_object(None)          # barrier: every writer has unmapped
+    for st in sets:
+        for ib in st.inboxes.values():
+            ib.free_home()
+        st.inboxes = {}
 
 
 # InboxSets kept per World (most recent programs); older ones are released
@@ -282,9 +311,14 @@ def inbox_set(prog, world, gpu_of) -> InboxSet:
     if not eligible_commits(prog, gpu_of):     # nothing to map: do not evict a useful set
         return _NO_INBOXES
     while len(reg) >= MAX_SETS:
-        # the least recently created set nobody pins (a CUDA graph or launch plan
-        # holding its raw pointers keeps it alive; then the registry grows)
-        victim = next((k for k, v in reg.items() if not getattr(v, "pins", 0)), None)
+        # the least recently created set no rank pins (a CUDA graph or launch plan
+        # holding its raw pointers keeps it alive; then the registry grows); the
+        # pin states are exchanged so every rank evicts the same set
+        pinned = [[k for k, v in reg.items() if getattr(v, "pins", 0)]]
+        if world.nprocs > 1:
+            pinned = world.all_gather_object(pinned[0])
+        held = {k for part in pinned for k in part}
+        victim = next((k for k in reg if k not in held), None)
         if victim is None:
             break
         reg.pop(victim).release(world)

@@ -368,11 +368,20 @@ class RegionStore:
 
     # ---- host views
     def gather(self, name: str) -> DenseTensor:
-        """Canonical value of a region on the host (D2H of the home pieces)."""
+        """Canonical value of a region on the host (D2H of the home pieces).
+
+        COLLECTIVE in SPMD jobs (one process per GPU): every piece is
+        broadcast from its holder, so every rank must call gather (or read
+        `RunResult.output`) at the same point -- calling it on rank 0 only
+        would leave rank 0 waiting for the others; the World.wait watchdog
+        then aborts NCCL and raises CommError after TD_NCCL_TIMEOUT seconds
+        instead of hanging.  Use `local_pieces` for rank-local reads."""
         torch = torch_mod()
         region = self.regions[name]
         out = np.zeros(region.dims, dtype=np.float64)
         W = self.world
+        if W.multi_gpu:
+            W.wait()
         for color, box, procs in region.dist.pieces():
             gpus = region.gpus_of(color)
             if not gpus:
@@ -462,6 +471,7 @@ def _bcast_piece(W, root_g, box, arr):
     st = torch.cuda.current_stream(dev)
     _native.call("td_bcast", W.comm(g), stream_handle(st), C.c_void_p(buf.data_ptr()),
                  max(1, box.volume), root_g)
+    W.wait()       # watchdog: a rank that never joins aborts the job instead of hanging it
     return buf.cpu().numpy()
 
 
@@ -1406,6 +1416,12 @@ class CapturedLaunch:
             store.zero(self.out)
         execute(stmt, store, record_requirements=False, leaf_policy=leaf_policy)
         torch.cuda.synchronize()
+        self.trace = plan_trace
+        if not _touches_owned(prog, store):
+            # this rank's GPUs hold no task, transfer or commit of the program: nothing
+            # to capture (an empty graph); replay() is a no-op here
+            self.graph = None
+            return
         self.graph = torch.cuda.CUDAGraph()
         _CAPTURING = True
         try:
@@ -1426,7 +1442,21 @@ class CapturedLaunch:
             weakref.finalize(self, iset.unpin)
 
     def replay(self) -> None:
-        self.graph.replay()
+        if self.graph is not None:
+            self.graph.replay()
+
+
+def _touches_owned(prog, store) -> bool:
+    """Does any task, transfer or commit of the program run on this process's GPUs?"""
+    W, m = store.world, store.machine
+
+    def mine(p):
+        return W.owns(m.device_of(p, W.ngpus))
+    if any(mine(t.coord) for t in prog.plan.tasks if t.out_rect is not None):
+        return True
+    if any(mine(t.src) or mine(t.dst) for moves in prog.transfers for t in moves):
+        return True
+    return any(mine(c.home) or mine(c.task.coord) for c in prog.commits)
 
 
 @dataclass
@@ -1438,6 +1468,7 @@ class RunResult:
 
     @property
     def output(self) -> DenseTensor:
+        """The output on the host (collective under SPMD: see RegionStore.gather)."""
         if self._output is None:
             self._output = self.store.gather(self.output_name)
         return self._output
