@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include <nccl.h>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -137,7 +138,9 @@ int td_comm_wait(void* const* comms, int ncomms, void* const* streams, int nstre
     }
     if (why) {
       // abort every communicator: pending NCCL kernels return, the job can shut down
+      if (std::getenv("TD_DEBUG")) std::fprintf(stderr, "td_comm_wait: %s; aborting %d comm(s)\n", why, ncomms);
       for (int k = 0; k < ncomms; ++k) ncclCommAbort(static_cast<ncclComm_t>(comms[k]));
+      if (std::getenv("TD_DEBUG")) std::fprintf(stderr, "td_comm_wait: aborted\n");
       td::set_error("comm_wait: %s; communicators aborted", why);
       return TD_ERR_NCCL;
     }

@@ -1,5 +1,5 @@
-"""NCCL watchdog check (2 ranks): rank 0 posts a send that rank 1 never
-receives.  World.wait must not hang: it polls ncclCommGetAsyncError, gives
+"""NCCL watchdog check (2 ranks): rank 0 posts a receive that rank 1 never
+sends.  World.wait must not hang: it polls ncclCommGetAsyncError, gives
 up after the timeout, aborts the communicators (ncclCommAbort) and raises
 CommError.  Run:  timeout 180 torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/nccl_watchdog_check.py
 """
@@ -26,17 +26,27 @@ def main():
     world = td.configure_distributed()
     rank = dist.get_rank()
     ok = True
-    if rank == 0:
-        g = world.owned[0]
-        buf = torch.ones(1 << 20, dtype=torch.float64, device=world.device(g))
-        st = world.streams(g)[1]
-        _native.call("td_send", world.comm(g), C.c_void_p(st.cuda_stream), C.c_void_p(buf.data_ptr()),
+    g = world.owned[0]
+    buf = torch.ones(1 << 20, dtype=torch.float64, device=world.device(g))
+    st = world.streams(g)[1]
+    # a matched pair first: NCCL connects peers lazily, and connection setup
+    # blocks on the host (not covered by the watchdog; NCCL_RUNTIME_CONNECT=0
+    # moves it into communicator creation)
+    for sender in (0, 1):       # both directions are separate connections
+        op = "td_send" if rank == sender else "td_recv"
+        _native.call(op, world.comm(g), C.c_void_p(st.cuda_stream), C.c_void_p(buf.data_ptr()), buf.numel(),
+                     1 - rank)
+        world.wait(timeout=60)
+    print(f"watchdog: rank {rank} warm-up pair done", flush=True)
+    if rank == 0:     # a receive whose data never comes: its NCCL kernel cannot finish
+        _native.call("td_recv", world.comm(g), C.c_void_p(st.cuda_stream), C.c_void_p(buf.data_ptr()),
                      buf.numel(), 1)
         t0 = time.time()
+        print("watchdog: waiting", flush=True)
         try:
             world.wait(timeout=5)
             ok = False
-            print("watchdog: wait returned although the send has no receiver", flush=True)
+            print("watchdog: wait returned although the receive has no sender", flush=True)
         except CommError as exc:
             print(f"watchdog: CommError after {time.time() - t0:.1f} s: {exc}", flush=True)
             ok = world.__dict__.get("broken", False)

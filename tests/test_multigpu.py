@@ -74,3 +74,13 @@ def test_spmd_torchrun_two_gpus():
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "tests", "mp_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "mp_check world=2: OK" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_nccl_watchdog_aborts_instead_of_hanging():
+    """A receive with no sender: World.wait gives up after its timeout, aborts
+    the communicators and raises CommError (tests/nccl_watchdog_check.py)."""
+    cmd = ["timeout", "180", sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "tests", "nccl_watchdog_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0 and "nccl_watchdog_check: OK" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
