@@ -1264,21 +1264,84 @@ def _plan_cached(stmt, store, trace, record_requirements):
     return prog
 
 
+# roofline denominators of `execute(timed=True)` (bench.py uses the same figures):
+# the FP64 DMMA peak measured on this pool's B200s (profiles/peaks_r01.json) and
+# the copy bandwidth of MEASURED_PEAKS.json
+FP64_PEAK_GFLOPS = 37070.0
+HBM_PEAK_GBS = 6544.3
+
+
+def _algorithmic_work(plan):
+    """(flop, bytes) of one launch of the statement: every iteration point of
+    the leaf does (#factors - 1) multiplications (+1 addition for a Reduce);
+    bytes = each distinct tensor read or written once."""
+    leaf = leaf_statements(plan.task_body)[0]
+    accs = [leaf.lhs, *accesses_of(leaf.rhs)]
+    ext = {}
+    for a in accs:
+        for v, d in zip(a.var_names, a.tensor.dims):
+            ext[v] = d
+    points = 1
+    for d in ext.values():
+        points *= d
+    nf = len(accesses_of(leaf.rhs))
+    flop = float(points) * (nf - 1 + (1 if plan.out_kind == "reduce" else 0))
+    vols = {}
+    for a in accs:
+        vol = 1
+        for d in a.tensor.dims:
+            vol *= d
+        vols[a.tensor.name] = vol
+    return flop, 8.0 * sum(vols.values())
+
+
 def execute(stmt, store: RegionStore, *, trace: ExecutionTrace = None, workers: int = 1,
-            label: str = None, record_requirements: bool = True, leaf_policy: str = "auto"):
+            label: str = None, record_requirements: bool = True, leaf_policy: str = "auto",
+            timed: bool = False):
     """Run one scheduled statement on the GPUs (reference `simulator.py:537-663`).
 
-    `workers` is accepted for signature compatibility; GPU parallelism
-    replaces the reference's thread pool.  `leaf_policy` is ``"auto"``
-    (native contractions where they apply) or ``"exact"`` (the nest kernel
-    everywhere: bitwise identical to the reference on any input)."""
+    `workers` is accepted for signature compatibility and has no effect: the
+    reference's thread pool over tasks (`simulator.py:617-620`) is replaced by
+    the GPUs themselves, and results do not depend on it (as in the
+    reference).  `leaf_policy` is ``"auto"`` (native contractions where they
+    apply) or ``"exact"`` (the nest kernel everywhere: bitwise identical to
+    the reference on any input).  `timed=True` brackets the launch with CUDA
+    events on every owned GPU, waits for it, and appends a record to
+    `trace.timings` (device ms, max over GPUs and ranks; algorithmic flop /
+    bytes; rate vs the FP64 or HBM roof), which `trace.stats()` reports under
+    "measured".  Collective under SPMD, like execute itself."""
     if leaf_policy not in LEAF_POLICIES:
         raise ConfigError(f"leaf_policy must be one of {LEAF_POLICIES}")
     if trace is None:
         trace = ExecutionTrace(store.machine)
     prog = _plan_cached(stmt, store, trace, record_requirements)
+    W = store.world
+    marks = None
+    if timed:
+        torch = torch_mod()
+        marks = {}
+        for g in W.owned:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(W.device(g)))
+            marks[g] = ev
     _launch(prog, store, leaf_policy)
     plan = prog.plan
+    if marks is not None:
+        ms = 0.0
+        for g, ev in marks.items():
+            end = torch.cuda.Event(enable_timing=True)
+            end.record(torch.cuda.current_stream(W.device(g)))
+            if W.multi_gpu:
+                W.wait()
+            end.synchronize()
+            ms = max(ms, ev.elapsed_time(end))
+        if W.nprocs > 1:
+            ms = max(W.all_gather_object(ms))
+        flop, nbytes = _algorithmic_work(plan)
+        tensor_bound = nbytes == 0 or flop / nbytes > FP64_PEAK_GFLOPS / HBM_PEAK_GBS
+        trace.record_timing(label or plan.out_name, ms, flops=flop, nbytes=nbytes,
+                            bound="tensor" if tensor_bound else "hbm",
+                            peak=FP64_PEAK_GFLOPS if tensor_bound else HBM_PEAK_GBS, gpus=W.ngpus)
     out_region = store[plan.out_name]
     out_region.zeroed = False
     if plan.out_kind == "reduce" and out_region.dist.replicated:
@@ -1508,13 +1571,14 @@ def prepare_store(cin, machine, distributions, inputs=None, *, world=None, gener
 
 
 def run_statement(stmt, machine: Machine, distributions: dict, inputs: dict, schedule=None, *,
-                  workers: int = 1, label: str = None, leaf_policy: str = "auto") -> RunResult:
+                  workers: int = 1, label: str = None, leaf_policy: str = "auto",
+                  timed: bool = False) -> RunResult:
     """Place inputs in HBM, apply the schedule, execute, return the output
-    (reference `simulator.py:676-715`)."""
+    (reference `simulator.py:676-715`).  `timed`: see `execute`."""
     cin = _scheduled(stmt, schedule)
     store, out_name = prepare_store(cin, machine, distributions, inputs)
     trace = ExecutionTrace(machine)
-    execute(cin, store, trace=trace, workers=workers, label=label, leaf_policy=leaf_policy)
+    execute(cin, store, trace=trace, workers=workers, label=label, leaf_policy=leaf_policy, timed=timed)
     return RunResult(out_name, trace, store)
 
 

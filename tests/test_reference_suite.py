@@ -2,7 +2,7 @@
 
 The reference's own tests are staged by `make ref` into oracle/_ref/tests
 (git-ignored, travels to the GPU box with the snapshot; read in place, never
-committed).  Every test module except the CLI ones is loaded with `tendist` and its
+committed).  Every test module, the CLI ones included (paper_2203_08069_b200.cli), is loaded with `tendist` and its
 submodules aliased to `paper_2203_08069_b200`, and each test function is run
 unmodified.  Tests that need values computed (run_statement, interpret,
 sequential_evaluate) raise DeviceUnavailable on a GPU-less host and are
@@ -23,15 +23,15 @@ import pytest
 from oracle.reference import tests_dir
 
 REF_TESTS = tests_dir()
-SKIP_FILES = {"test_cli.py", "test_acceptance.py"}    # exercise the reference CLI (out of scope)
+SKIP_FILES = set()
 
 
 def _alias():
     import paper_2203_08069_b200 as pkg
-    from paper_2203_08069_b200 import (cin, distribution, errors, ir, machine, scheduling, tensors)
-    mods = {"tendist": pkg, "tendist.cin": cin, "tendist.distribution": distribution, "tendist.errors": errors,
-            "tendist.ir": ir, "tendist.machine": machine, "tendist.scheduling": scheduling,
-            "tendist.tensors": tensors}
+    from paper_2203_08069_b200 import (cin, cli, distribution, errors, ir, machine, scheduling, tensors)
+    mods = {"tendist": pkg, "tendist.cin": cin, "tendist.cli": cli, "tendist.distribution": distribution,
+            "tendist.errors": errors, "tendist.ir": ir, "tendist.machine": machine,
+            "tendist.scheduling": scheduling, "tendist.tensors": tensors}
     saved = {k: sys.modules.get(k) for k in mods}
     sys.modules.update(mods)
     return saved

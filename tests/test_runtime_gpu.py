@@ -218,3 +218,34 @@ def test_native_leaves_are_used_for_bundles():
         res, ins = b.run(seed=1)
         assert leaves.STATS[kind] > 0 and leaves.STATS["nest"] == 0, (b.name, leaves.STATS)
         td.verify_result(b.statement, ins, res)
+
+
+def test_timed_launch_fills_measured_stats(tmp_path):
+    """execute(timed=True): trace.timings gets the launch's device time and
+    algorithmic work; stats() reports it under "measured" beside the
+    reference schema (which is otherwise unchanged)."""
+    b = td.cannon(1, 1, dims=(1024, 1024, 1024))
+    res, _ = b.run(seed=1, timed=True)
+    st = res.trace.stats({"algorithm": "cannon"})
+    m = st["measured"]
+    (row,) = m["launches"]
+    assert row["flops"] == 2.0 * 1024 ** 3 and row["bound"] == "tensor" and row["device_ms"] > 0
+    assert row["rate_unit"] == "GFLOP/s" and 0 < row["frac_of_peak"] < 1.2
+    t = td.ttv(1, dims=(256, 256, 256))
+    res, _ = t.run(seed=1, timed=True)
+    (row,) = res.trace.stats()["measured"]["launches"]
+    assert row["bound"] == "hbm" and row["rate_unit"] == "GB/s"
+    untimed, _ = b.run(seed=1)
+    assert "measured" not in untimed.trace.stats()
+
+
+def test_cli_timing_and_stats(tmp_path, capsys):
+    from paper_2203_08069_b200 import cli
+    path = tmp_path / "s.json"
+    assert cli.main(["--algorithm", "summa", "--dims", "512x512x512", "--chunk", "64", "--timing", "--verify",
+                     "--stats", str(path)]) == 0
+    out = capsys.readouterr().out
+    assert "verify: OK" in out and "% of the tensor roof" in out
+    import json
+    stats = json.loads(path.read_text())
+    assert stats["measured"]["launches"][0]["device_ms"] > 0
