@@ -26,6 +26,7 @@ Drop-in for the reference's runtime (`pkg/src/tendist/simulator.py`):
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -223,6 +224,10 @@ class RegionStore:
             (order,) = struct.unpack("<Q", head)
             dims = struct.unpack("<" + "Q" * order, fh.read(8 * order)) if order else ()
         self._check(name, dims, dist)
+        need = 8 * (1 + order) + 8 * (int(np.prod(dims, dtype=np.int64)) if dims else 1)
+        have = os.path.getsize(path)
+        if have != need:     # as the reference's from_bytes (tensors.py:84-92): short or long payloads fail
+            raise ExtentMismatch(f"{path}: {have} bytes, but a tensor of dims {tuple(dims)} needs {need}")
         payload = np.memmap(path, dtype="<f8", mode="r", offset=8 * (1 + order),
                             shape=tuple(dims) if dims else (1,))
 

@@ -249,3 +249,22 @@ def test_cli_timing_and_stats(tmp_path, capsys):
     import json
     stats = json.loads(path.read_text())
     assert stats["measured"]["launches"][0]["device_ms"] > 0
+
+
+def test_place_file_rejects_wrong_payload_size(tmp_path):
+    """A file whose payload disagrees with its header dims fails with
+    ExtentMismatch, as the reference's from_bytes does (tensors.py:84-92)."""
+    from paper_2203_08069_b200.errors import ExtentMismatch
+    t = td.DenseTensor((4, 6), np.arange(24, dtype=float).reshape(4, 6))
+    good = tmp_path / "t.bin"
+    td.save_tensor(t, good)
+    raw = good.read_bytes()
+    b = td.summa(2, 2, dims=(4, 6, 6))
+    store = td.RegionStore(b.machine)
+    for bad in (raw[:-8], raw + b"\0" * 8):
+        p = tmp_path / "bad.bin"
+        p.write_bytes(bad)
+        with pytest.raises(ExtentMismatch):
+            store.place_file("A", p, b.distributions["A"])
+    store.place_file("A", good, b.distributions["A"])
+    assert store["A"].tensor == t
