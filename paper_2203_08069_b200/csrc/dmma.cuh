@@ -3,7 +3,7 @@
 // sm_100a has no FP64 form of tcgen05.mma (ptxas: "Unknown modifier
 // '.kind::f64'") and wgmma is sm_90a-only, so the FP64 tensor path on B200 is
 // the warp-level `mma.sync.aligned.m8n8k4.f64` (SASS: DMMA.8x8x4).  Measured on
-// this pool's B200 (scratch/dmma.cu): 37.06 TFLOP/s at 1965 MHz, i.e. the full
+// this pool's B200 (tools/tuning/dmma.cu): 37.06 TFLOP/s at 1965 MHz, i.e. the full
 // 148 SM x 128 flop/clk FP64 peak, identical to DFMA.  Operands are staged
 // through shared memory by TMA bulk tensor copies (gemm_tma.cuh, the default
 // wherever the copy engine can address the operands) or by cp.async (LDGSTS)

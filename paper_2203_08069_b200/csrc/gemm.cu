@@ -297,7 +297,7 @@ static int raster_group(int blocks_per_sm, int BM, int BN) {
     return e ? std::atoi(e) : 0;
   }();
   if (forced > 0) return forced;
-  // Measured on B200 at 16384^3 with 64x64 tiles (scratch/group_sweep.sh):
+  // Measured on B200 at 16384^3 with 64x64 tiles (tools/tuning/group_sweep.sh):
   // DRAM read per launch 558/290/164/115/128/263 GB for groups 1/2/4/8/16/32
   // with the same 35.5 TFLOP/s -- 8 M-tiles per group minimises re-reads.
   (void)blocks_per_sm;
@@ -403,7 +403,7 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(48, 128, 32, 16, 32, 32, 3, 4)             \
   X(50, 128, 64, 16, 64, 32, 4, 0)
 
-// Tile history on B200 (scratch/tune2.py, tune_n32.py, tune_n64.py; 16384^3
+// Tile history on B200 (tools/tuning/tune2.py, tune_n32.py, tune_n64.py; 16384^3
 // unless noted):
 //   LDGSTS 128x64x16, 4 warps of 64x32, 3 stages, 2 CTAs/SM          34.2 TFLOP/s
 //   + fixed-address load path, 64x128x16 (cuBLAS's own d884 tile)       35.2

@@ -391,7 +391,7 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
   // default 18: the TMA-fed GEMM body on 128x32x16 tiles, 3 stages, <= 128
   // registers -> 34.8 TFLOP/s at 1024^3 r32 (LDGSTS body, config 12: 33.4; fused
-  // kernel, best config 6: 30.9; scratch/tune_n32.py).  Operands the copy
+  // kernel, best config 6: 30.9; tools/tuning/tune_n32.py).  Operands the copy
   // engine cannot address take the LDGSTS body with the same tile.
   switch (config < 0 ? 18 : config) {
     case 0: return launch_mttkrp<4, 4, 1, 16, false, 2>(st, a, vec2);

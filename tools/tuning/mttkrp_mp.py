@@ -1,6 +1,6 @@
 """MTTKRP weak-scaled step time under torchrun: where the multi-GPU overhead goes.
 
-    torchrun --nproc-per-node 4 scratch/mttkrp_mp.py
+    torchrun --nproc-per-node 4 tools/tuning/mttkrp_mp.py
 """
 import os
 import sys

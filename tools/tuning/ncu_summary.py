@@ -17,7 +17,11 @@ WANT = {
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1, "second": 1e3}
 out = {}
-for name, rep in [("dgemm", "dgemm"), ("ttv", "ttv"), ("innerprod", "innerprod"), ("ttm", "ttm"), ("mttkrp", "mttkrp")]:
+import os
+for name, rep in [("dgemm", "dgemm"), ("ttv", "ttv"), ("innerprod", "innerprod"), ("ttm", "ttm"), ("mttkrp", "mttkrp"),
+                  ("g1_grouped", "g1")]:
+    if not os.path.exists(f"gpurun_out/{R}_{rep}.ncu-rep"):
+        continue
     raw = subprocess.run(["ncu", "-i", f"gpurun_out/{R}_{rep}.ncu-rep", "--page", "raw", "--csv"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -42,7 +46,7 @@ for name, rep in [("dgemm", "dgemm"), ("ttv", "ttv"), ("innerprod", "innerprod")
     d["stall_share_top"] = {k: round(v / tot, 3) for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:5]}
     d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
     out[name] = d
-out["_note"] = ("ncu --set full --clock-control none on one bench-size launch (scratch/prof2.py); "
+out["_note"] = ("ncu --set full --clock-control none on one bench-size launch (tools/tuning/prof2.py); "
                 "cold-cache, serialised replay: compare shares, not absolute times")
 json.dump(out, open(f"profiles/ncu_summary_{R}.json", "w"), indent=1)
 for k, v in out.items():

@@ -1,6 +1,6 @@
 """GEMM -> reduce over peer memory vs NCCL write-back (torchrun, N GPUs).
 
-    torchrun --nproc-per-node 2 scratch/peer_bench.py [n]
+    torchrun --nproc-per-node 2 tools/tuning/peer_bench.py [n]
 """
 import os
 import sys

@@ -1,6 +1,6 @@
 # bench-size launches of each native leaf (one warm-up + one profiled), for ncu
 import ctypes as C, sys
-sys.path.insert(0, ".")
+sys.path.insert(0, ".")  # run from the repo root
 import torch
 from paper_2203_08069_b200 import _native as nat
 nat.load()
@@ -28,6 +28,15 @@ elif which == "ttm":
     n, L = 1024, 64
     b = gen((n, n, n), 1); cm = gen((n, L), 2); y = torch.empty(n, n, L, dtype=torch.float64, device="cuda")
     for _ in range(2): nat.call("td_ttm", st(), n, n, n, L, P(b), n*n, n, P(cm), L, P(y), n*L, L, 0)
+elif which == "g1":
+    # BASELINE G1 (SUMMA 1024^3 on 2x2, chunk 128) through the runtime: launch plans
+    # replay its 2 grouped k-merged DMMA launches (dgemm_tma_grouped_kernel)
+    import paper_2203_08069_b200 as td
+    b = td.summa(2, 2, dims=(1024,) * 3, chunk=128)
+    cin, store = b.prepare(seed=0, mode=0)
+    for _ in range(4):
+        store.zero("C")
+        td.execute(cin, store, record_requirements=False)
 elif which == "mttkrp":
     n, R = 1024, 32
     b = gen((n, n, n), 1); cm = gen((n, R), 2); d = gen((n, R), 3); a = torch.empty(n, R, dtype=torch.float64, device="cuda")
