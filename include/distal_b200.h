@@ -50,6 +50,12 @@ int td_device_count(void);
 int td_set_device(int device);
 /* Number of kernel launches this library issued since load (all threads). */
 long long td_launch_count(void);
+/* Lifecycle: create the CUDA contexts of `devices` up front; drain every
+ * device (host-visible completion) at the end.  Communicators are created
+ * with td_comm_init_rank / td_comm_init_all (+ td_comm_split for the axis
+ * sub-communicators of a processor grid) and freed with td_comm_destroy. */
+int td_init(int ndev, const int* devices);
+int td_finalize(void);
 /* Device ordinal a stream belongs to (every compute entry point makes that
  * device current for the call, so one thread can drive several GPUs). */
 int td_stream_device(void* stream);
@@ -187,6 +193,12 @@ int td_recv(void* comm, void* stream, double* buf, int64_t count, int peer);
 int td_bcast(void* comm, void* stream, double* buf, int64_t count, int root);
 int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count, int root);
 int td_allreduce_sum(void* comm, void* stream, const double* send, double* recv, int64_t count);
+/* recv[r*count ..] = send of rank r (SUMMA's row-panel gather along a grid axis). */
+int td_allgather(void* comm, void* stream, const double* send, double* recv, int64_t count);
+/* Cyclic shift along the communicator's ring: send to rank+delta, receive
+ * from rank-delta (mod size) -- Cannon's systolic step, rotate() of
+ * scheduling.py:222-260. */
+int td_shift(void* comm, void* stream, const double* send, double* recv, int64_t count, int delta);
 /* Host-side wait with a watchdog: returns when every stream is idle; while
  * waiting polls ncclCommGetAsyncError on every communicator, and on an async
  * error or after timeout_s seconds (<= 0: never) aborts ALL of them

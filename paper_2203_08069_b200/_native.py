@@ -72,6 +72,10 @@ _SIGNATURES = {
     "td_stream_wait_event": ([vp, vp, i32], i32),
     "td_execute_plan": ([vp, i64], i32),
     "td_comm_wait": ([C.POINTER(vp), i32, C.POINTER(vp), i32, C.c_double], i32),
+    "td_init": ([i32, C.POINTER(C.c_int)], i32),
+    "td_finalize": ([], i32),
+    "td_allgather": ([vp, vp, dp, dp, i64], i32),
+    "td_shift": ([vp, vp, dp, dp, i64, i32], i32),
 }
 
 EXPORTED = tuple(_SIGNATURES)

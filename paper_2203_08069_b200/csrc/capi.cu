@@ -42,6 +42,34 @@ int td_set_device(int device) {
 
 long long td_launch_count(void) { return td::g_launches.load(); }
 
+int td_init(int ndev, const int* devices) {
+  TD_REQUIRE(ndev >= 0 && (ndev == 0 || devices), "init: bad device list");
+  int prev = 0;
+  TD_CUDA(cudaGetDevice(&prev));
+  for (int k = 0; k < ndev; ++k) {  // create the primary contexts up front (not inside the first launch)
+    TD_CUDA(cudaSetDevice(devices[k]));
+    TD_CUDA(cudaFree(nullptr));
+  }
+  TD_CUDA(cudaSetDevice(prev));
+  return TD_OK;
+}
+
+int td_finalize(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return TD_OK;
+  }
+  int prev = 0;
+  TD_CUDA(cudaGetDevice(&prev));
+  for (int d = 0; d < n; ++d) {  // drain every device this process touched
+    TD_CUDA(cudaSetDevice(d));
+    TD_CUDA(cudaDeviceSynchronize());
+  }
+  TD_CUDA(cudaSetDevice(prev));
+  return TD_OK;
+}
+
 int td_stream_device(void* stream) {
   int dev = -1;
   TD_CUDA(cudaStreamGetDevice(td::as_stream(stream), &dev));

@@ -105,6 +105,33 @@ int td_reduce_sum(void* comm, void* stream, const double* send, double* recv, in
   return TD_OK;
 }
 
+int td_allgather(void* comm, void* stream, const double* send, double* recv, int64_t count) {
+  TD_NCCL(ncclAllGather(send, recv, (size_t)count, ncclDouble, static_cast<ncclComm_t>(comm),
+                        td::as_stream(stream)));
+  return TD_OK;
+}
+
+int td_shift(void* comm, void* stream, const double* send, double* recv, int64_t count, int delta) {
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  int n = 0, me = 0;
+  TD_NCCL(ncclCommCount(c, &n));
+  TD_NCCL(ncclCommUserRank(c, &me));
+  const int to = ((me + delta) % n + n) % n;
+  const int from = ((me - delta) % n + n) % n;
+  if (to == me) {  // a shift by a multiple of the ring: a local copy
+    if (send != recv)
+      TD_CUDA(cudaMemcpyAsync(recv, send, size_t(count) * 8, cudaMemcpyDeviceToDevice, td::as_stream(stream)));
+    return TD_OK;
+  }
+  TD_NCCL(ncclGroupStart());
+  ncclResult_t r1 = ncclSend(send, (size_t)count, ncclDouble, to, c, td::as_stream(stream));
+  ncclResult_t r2 = ncclRecv(recv, (size_t)count, ncclDouble, from, c, td::as_stream(stream));
+  TD_NCCL(ncclGroupEnd());
+  TD_NCCL(r1);
+  TD_NCCL(r2);
+  return TD_OK;
+}
+
 int td_comm_wait(void* const* comms, int ncomms, void* const* streams, int nstreams, double timeout_s) {
   TD_REQUIRE((ncomms == 0 || comms) && (nstreams == 0 || streams), "comm_wait: null arrays");
   const auto t0 = std::chrono::steady_clock::now();
