@@ -84,3 +84,44 @@ def test_nccl_watchdog_aborts_instead_of_hanging():
            "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "tests", "nccl_watchdog_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert out.returncode == 0 and "nccl_watchdog_check: OK" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_abi_collectives_allgather_and_shift():
+    """td_allgather / td_shift (§8(b) ABI) on a one-process clique of the visible GPUs."""
+    code = r"""
+import ctypes as C, sys, torch
+sys.path.insert(0, %r)
+from paper_2203_08069_b200 import _native as nat
+lib = nat.load()
+n = min(4, torch.cuda.device_count())
+devs = (C.c_int * n)(*range(n))
+assert lib.td_init(n, devs) == 0
+comms = (C.c_void_p * n)()
+nat.call("td_comm_init_all", comms, n, devs)
+cnt = 1000
+send = [torch.full((cnt,), float(r + 1), dtype=torch.float64, device=f"cuda:{r}") for r in range(n)]
+gath = [torch.zeros(n * cnt, dtype=torch.float64, device=f"cuda:{r}") for r in range(n)]
+shf = [torch.zeros(cnt, dtype=torch.float64, device=f"cuda:{r}") for r in range(n)]
+sts = [torch.cuda.current_stream(r).cuda_stream for r in range(n)]
+nat.call("td_group_start")
+for r in range(n):
+    nat.call("td_allgather", C.c_void_p(comms[r]), C.c_void_p(sts[r]), C.c_void_p(send[r].data_ptr()),
+             C.c_void_p(gath[r].data_ptr()), cnt)
+nat.call("td_group_end")
+nat.call("td_group_start")
+for r in range(n):
+    nat.call("td_shift", C.c_void_p(comms[r]), C.c_void_p(sts[r]), C.c_void_p(send[r].data_ptr()),
+             C.c_void_p(shf[r].data_ptr()), cnt, 1)
+nat.call("td_group_end")
+assert lib.td_finalize() == 0
+for r in range(n):
+    want = torch.cat([torch.full((cnt,), float(q + 1), dtype=torch.float64) for q in range(n)])
+    assert torch.equal(gath[r].cpu(), want), r
+    assert torch.equal(shf[r].cpu(), torch.full((cnt,), float((r - 1) %% n + 1), dtype=torch.float64)), r
+for r in range(n):
+    nat.call("td_comm_destroy", C.c_void_p(comms[r]))
+print("abi collectives OK")
+""" % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "abi collectives OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
