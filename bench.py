@@ -192,7 +192,12 @@ def _leaf_timing(td, kind):
 
 
 def _profile_traffic(name):
-    path = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    """DRAM bytes per launch of the kernel from the latest committed ncu capture."""
+    import glob
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")))
+    if not found:
+        return None
+    path = found[-1]
     try:
         with open(path) as fh:
             return json.load(fh).get(name, {}).get("dram_bytes_per_launch")
