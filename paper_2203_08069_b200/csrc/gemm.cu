@@ -418,6 +418,13 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // 34.3, 64x32 with 16x32 warps 35.1; and the MTTKRP tail wave split into
 // half-k CTAs 34.8-35.1 (CTA waves are not synchronous); a persistent
 // row-sum kernel keeping the TMA ring running across tiles 31.0-31.7.
+// Round 2 (tools/kernel_probe.py): the tail of the last wave costs MTTKRP
+// ~1.7 % at I = 1024 (35.0 TFLOP/s; 35.3 at I = 999 = 18 full waves, 35.6
+// at I = 4096), and a persistent TMA kernel with dynamically claimed tiles
+// (atomic counter, claim latency hidden one tile ahead, the ring running
+// across tile boundaries, both EPI forms) measured 33.8 (MTTKRP) and 35.8
+// (TTM) against 35.0 / 36.1 here: co-resident CTAs already hide a new
+// tile's cold pipeline, so the per-tile CTAs stay.
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;

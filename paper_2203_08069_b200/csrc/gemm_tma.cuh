@@ -63,6 +63,107 @@ struct TmaCfg {
   static_assert(BK % 4 == 0 && BN % 8 == 0 && BM <= 256 && BK * BN / 4 <= 256 * 64, "tma tile");
 };
 
+// Epilogue of one tile: EPI = 0 stores (or accumulates) the accumulators
+// into C; EPI = 1 (MTTKRP) multiplies by H, sums the tile's rows in a fixed
+// order through `red` (WARPS_M x BN doubles of shared memory) into the
+// workspace row of the M-tile, and with p.counters the last CTA of the
+// (batch, N-tile) finishes the ordered sum over the M-tiles.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB>
+__device__ __forceinline__ void tma_epilogue(double (&acc)[TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::FM]
+                                                           [TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::FN][2],
+                                             const GemmArgs& p, double* __restrict__ C, const int tm, const int tn,
+                                             const int m0, const int n0, const int bz, double* red) {
+  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
+  const int64_t M = p.M, N = p.N;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp / Cfg::WARPS_N) * WM;
+  const int wn0 = (warp % Cfg::WARPS_N) * WN;
+  if constexpr (EPI == 1) {  // MTTKRP row-sum epilogue (see dgemm_kernel)
+    double part[Cfg::FN][2];
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) part[j][0] = part[j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) {
+      const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+      const double* hrow = p.H + r * p.ldh;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (r < M && c + h < N) part[j][h] += hrow[c + h] * acc[i][j][h];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = part[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        part[j][h] = v;
+      }
+    if (lane < 4) {
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) red[(warp / Cfg::WARPS_N) * BN + wn0 + j * 8 + lane * 2 + h] = part[j][h];
+    }
+    __syncthreads();
+    for (int c = tid; c < BN; c += Cfg::THREADS) {
+      double v = red[c];
+#pragma unroll
+      for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
+      if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
+    }
+    if (p.counters != nullptr) {
+      // fused finish (replaces mttkrp_reduce): the last CTA of this (batch, N-tile)
+      // to arrive sums the M-tile partials in ascending order -- the same order,
+      // so the same bits -- and writes the output row
+      __shared__ int last_arrival;
+      __threadfence();
+      __syncthreads();
+      int* counter = p.counters + int64_t(bz) * p.N + tn;
+      if (tid == 0) last_arrival = atomicAdd(counter, 1) == p.tiles_m - 1;
+      __syncthreads();
+      if (last_arrival) {
+        __threadfence();
+        for (int c = tid; c < BN; c += Cfg::THREADS) {
+          if (n0 + c >= N) continue;
+          double v = 0.0;
+          for (int g = 0; g < p.tiles_m; ++g) v += __ldcg(C + int64_t(g) * N + n0 + c);
+          double* dst = p.out + int64_t(bz) * p.ldo + n0 + c;
+          *dst = p.out_acc ? *dst + v : v;
+        }
+        if (tid == 0) *counter = 0;  // ready for the next launch on this workspace
+      }
+    }
+    return;
+  }
+
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
+    if (r >= M) continue;
+    double* crow = C + r * p.ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h < N) {
+          double v = acc[i][j][h];
+          if (p.accumulate) v += crow[c + h];
+          crow[c + h] = v;
+        }
+      }
+    }
+  }
+}
+
 // One CTA tile of the TMA-fed GEMM: tile `tile` (raster order) of batch
 // entry `bz`, operands through the tensor maps tmA / tmB (kernel-parameter
 // addresses: __grid_constant__).  Shared by the plain kernel and the
@@ -148,90 +249,8 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
     }
   }
 
-  if constexpr (EPI == 1) {  // MTTKRP row-sum epilogue (see dgemm_kernel)
-    double part[Cfg::FN][2];
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j) part[j][0] = part[j][1] = 0.0;
-#pragma unroll
-    for (int i = 0; i < Cfg::FM; ++i) {
-      const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
-      const double* hrow = p.H + r * p.ldh;
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) {
-        const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (r < M && c + h < N) part[j][h] += hrow[c + h] * acc[i][j][h];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double v = part[j][h];
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        part[j][h] = v;
-      }
-    __syncthreads();  // every stage has been consumed: reuse the ring as [WARPS_M][BN]
-    double* red = smem;
-    if (lane < 4) {
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) red[(warp / Cfg::WARPS_N) * BN + wn0 + j * 8 + lane * 2 + h] = part[j][h];
-    }
-    __syncthreads();
-    for (int c = tid; c < BN; c += Cfg::THREADS) {
-      double v = red[c];
-#pragma unroll
-      for (int w = 1; w < Cfg::WARPS_M; ++w) v += red[w * BN + c];
-      if (n0 + c < N) C[int64_t(tm) * N + n0 + c] = v;
-    }
-    if (p.counters != nullptr) {
-      // fused finish (replaces mttkrp_reduce): the last CTA of this (batch, N-tile)
-      // to arrive sums the M-tile partials in ascending order -- the same order,
-      // so the same bits -- and writes the output row
-      __shared__ int last_arrival;
-      __threadfence();
-      __syncthreads();
-      int* counter = p.counters + int64_t(bz) * p.N + tn;
-      if (tid == 0) last_arrival = atomicAdd(counter, 1) == p.tiles_m - 1;
-      __syncthreads();
-      if (last_arrival) {
-        __threadfence();
-        for (int c = tid; c < BN; c += Cfg::THREADS) {
-          if (n0 + c >= N) continue;
-          double v = 0.0;
-          for (int g = 0; g < p.tiles_m; ++g) v += __ldcg(C + int64_t(g) * N + n0 + c);
-          double* dst = p.out + int64_t(bz) * p.ldo + n0 + c;
-          *dst = p.out_acc ? *dst + v : v;
-        }
-        if (tid == 0) *counter = 0;  // ready for the next launch on this workspace
-      }
-    }
-    return;
-  }
-
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i) {
-    const int64_t r = m0 + wm0 + i * 8 + (lane >> 2);
-    if (r >= M) continue;
-    double* crow = C + r * p.ldc;
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j) {
-      const int64_t c = n0 + wn0 + j * 8 + (lane & 3) * 2;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (c + h < N) {
-          double v = acc[i][j][h];
-          if (p.accumulate) v += crow[c + h];
-          crow[c + h] = v;
-        }
-      }
-    }
-  }
+  if constexpr (EPI == 1) __syncthreads();  // every stage has been consumed: the ring serves as scratch
+  tma_epilogue<BM, BN, BK, WM, WN, STAGES, EPI, MINB>(acc, p, C, tm, tn, m0, n0, bz, smem);
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB = 0>
@@ -349,3 +368,4 @@ static int launch_gemm_tma_grouped(cudaStream_t st, int count, const GemmArgs* p
 }
 
 }  // namespace td
+
