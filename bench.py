@@ -269,8 +269,10 @@ def bench_gemm(job, steps, warmup, e2e_steps):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
                      "traffic": _profile_traffic("dgemm"),
-                     "peak_source": "measured FP64 DMMA probe (profiles/peaks_r01.json); "
-                                    f"cuBLAS DGEMM on the same GPUs: {DGEMM_CUBLAS_TFLOPS} TFLOP/s",
+                     "peak_source": "builder-measured FP64 DMMA probe (profiles/peaks_r01.json; MEASURED_PEAKS.json "
+                                    "has no FP64 entry); cuBLAS DGEMM on the same GPUs: "
+                                    f"{DGEMM_CUBLAS_TFLOPS} TFLOP/s",
+                     "frac_of_cublas_dgemm": (achieved / DGEMM_CUBLAS_TFLOPS) if achieved else None,
                      "flop_per_launch": flop_per_launch},
         "clocks": clk.summary(), "e2e": e2e, "overlap": overlap,
     }
@@ -420,6 +422,10 @@ def bench_gemm_e2e(job, bundle, cin, steps):
     return {"value": flop * steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(job.sum_over_ranks(h2d)),
             "d2h_bytes_per_step": int(job.sum_over_ranks(d2h)), "ms_per_step": dt * 1e3 / steps,
             "steps": steps, "algorithm": f"{bundle.name} {bundle.machine}", "rows_exact": ok,
+            "algorithm_note": ("p = 1: the same 16384^3 GEMM as SUMMA on a 4x1 grid placed on the one GPU (4 row "
+                               "blocks x 8 k-chunks), so the upload of later k-slabs and the download of finished "
+                               "row blocks overlap the DMMA leaves; the device-resident `value` runs Cannon 1x1")
+            if bundle.machine.size == 4 and job.world.ngpus == 1 else "the headline algorithm",
             "how": "pinned host pieces -> RegionStore.place_local (async H2D in k-slabs on two copy streams; "
                    "leaves and NCCL sends wait only for the slabs they touch: p=1 task-major k-chunks, p>1 "
                    "the pipelined first step in the A upload's 8 k-slabs) -> execute -> D2H of output rows as "
@@ -663,7 +669,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="all", choices=["all", "gemm"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--procs", type=int, default=0,
                     help="logical processors of the BASELINE layout (default: one per GPU)")
@@ -672,7 +678,7 @@ def main():
         run_reference_arm(args)
         return
     job = Job(args.gpus, args.procs)
-    gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps)
+    gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps or args.steps)
     kernels = bench_kernels(job, max(2, args.steps // 2), max(3, args.warmup)) if args.workload == "all" else None
     if job.rank == 0:
         report(args, job, gemm, kernels)
