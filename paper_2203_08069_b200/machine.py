@@ -10,7 +10,11 @@ B200 mapping: one NVSwitch box is a single flat level, so a hierarchical
 machine executes as its flattened grid (levels only matter for the stats
 split).  `device_of` places processor ``rank`` on GPU
 ``rank * ndev // size`` -- identity when the grid has exactly one processor
-per GPU, contiguous blocks of processors per GPU when oversubscribed.
+per GPU, contiguous blocks of processors per GPU when oversubscribed
+(placement "block", the default).  `set_placement("cyclic")` deals the
+processors round robin instead (``rank % ndev``), which e.g. puts Johnson's
+depth pairs on different GPUs; choose it before placing data (it decides
+where every piece lives).
 """
 
 from __future__ import annotations
@@ -19,6 +23,21 @@ import itertools
 from functools import reduce
 
 from .errors import ConfigError, EmptyGrid
+
+PLACEMENTS = ("block", "cyclic")
+_PLACEMENT = "block"
+
+
+def set_placement(policy: str) -> None:
+    """Processor -> GPU mapping of oversubscribed grids: "block" or "cyclic"."""
+    global _PLACEMENT
+    if policy not in PLACEMENTS:
+        raise ConfigError(f"placement must be one of {PLACEMENTS}, got {policy!r}")
+    _PLACEMENT = policy
+
+
+def placement() -> str:
+    return _PLACEMENT
 
 
 class Machine:
@@ -86,7 +105,10 @@ class Machine:
 
     def device_of(self, coord, ndev: int) -> int:
         """GPU ordinal (in the job's device list) that runs processor coord."""
-        return self.rank_of(coord) * ndev // self.size if ndev < self.size else self.rank_of(coord)
+        r = self.rank_of(coord)
+        if ndev >= self.size:
+            return r
+        return r % ndev if _PLACEMENT == "cyclic" else r * ndev // self.size
 
 
 def make_machine(levels) -> Machine:

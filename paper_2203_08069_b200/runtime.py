@@ -1244,7 +1244,8 @@ def _plan_cached(stmt, store, trace, record_requirements):
     iterative solvers) skip the Python planning and replay its ledger."""
     # the program depends on the distributions and residency only, not on the
     # store object or its values: key on those so fresh stores (e2e steps) hit
-    layout = (store.machine, store.world.ngpus,
+    from .machine import placement
+    layout = (store.machine, store.world.ngpus, placement(),
               tuple((n, r.dist, tuple(len(v) for v in r.residency.values()))
                     for n, r in sorted(store.regions.items())))
     cache = _PLAN_CACHE

@@ -76,6 +76,29 @@ def main():
         if not np.array_equal(res.output.data, np.asarray(want)):
             failures.append(f"8-proc {b.name} {b.machine}")
 
+    # Johnson 2x2x2 with its depth pairs on different GPUs (cyclic placement at 4 GPUs, as at 8):
+    # the depth partials travel through peer inboxes, eagerly and from replayed launch plans
+    if size == 4:
+        from paper_2203_08069_b200 import machine as mach
+        mach.set_placement("cyclic")
+        try:
+            b = td.johnson(2, 2, 2, dims=(128, 96, 160))
+            cin, store = b.prepare(seed=17, mode=0, world=world)
+            ins = {n: generate(b.statement.tensors()[n].dims, 17, k + 1, 0) for k, n in enumerate(b.input_names)}
+            want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+            for rep in range(4):
+                store.zero("C")
+                td.execute(cin, store)
+                if not np.array_equal(store["C"].tensor.data, want):
+                    failures.append(f"johnson cyclic run {rep}")
+            used = sum(len(s.inboxes) for s in world.inbox_sets.values())
+            if used == 0:
+                failures.append("johnson cyclic: no peer inbox used")
+            if rank == 0:
+                print(f"peer johnson 2x2x2 (cyclic on {size} GPUs): inboxes in use {used}", flush=True)
+        finally:
+            mach.set_placement("block")
+
     # launch plans under SPMD: each rank records its own ops (NCCL groups, peer-inbox tokens and
     # credits, leaves) on the second execute and replays them from the third
     from paper_2203_08069_b200 import runtime as rt
