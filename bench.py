@@ -673,10 +673,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--procs", type=int, default=0,
                     help="logical processors of the BASELINE layout (default: one per GPU)")
+    ap.add_argument("--placement", default="block", choices=("block", "cyclic"),
+                    help="processor -> GPU mapping when --procs exceeds the GPUs (Machine.device_of)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    from paper_2203_08069_b200 import machine as _machine
+    _machine.set_placement(args.placement)
     job = Job(args.gpus, args.procs)
     gemm = bench_gemm(job, args.steps, args.warmup, args.e2e_steps or args.steps)
     kernels = bench_kernels(job, max(2, args.steps // 2), max(3, args.warmup)) if args.workload == "all" else None
@@ -690,7 +694,11 @@ def gemm_config(td, p, gpus=None):
     n = td.weak_gemm_n(p)
     b = td.gemm_for_gpus(p, n)
     gpus = gpus or p
-    par = f"{p} GPU(s), one task per GPU" if gpus == p else f"{p} processors on {gpus} GPUs"
+    if gpus == p:
+        par = f"{p} GPU(s), one task per GPU"
+    else:
+        from paper_2203_08069_b200.machine import placement
+        par = f"{p} processors on {gpus} GPUs ({placement()} placement)"
     return {"workload": f"fp64 GEMM {n}^3 weak-scaled from 16384^3 ({b.name} on {b.machine})", "n": n,
             "algorithm": b.name, "grid": str(b.machine), "parallelism": par,
             "l2": "inputs (>= 2 GiB per operand) exceed the 126 MB L2; no flush needed",
