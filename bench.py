@@ -258,8 +258,7 @@ def bench_gemm(job, steps, warmup, e2e_steps):
     del store, step
     gc.collect()
     torch.cuda.empty_cache()
-    e2e = bench_gemm_e2e(job, bundle, cin, e2e_steps) if job.procs == job.n_gpus else {
-        "value": None, "unit": "GFLOP/s", "note": f"{job.procs} processors on {job.n_gpus} GPUs: device-resident only"}
+    e2e = bench_gemm_e2e(job, bundle, cin, e2e_steps)
     gc.collect()
     torch.cuda.empty_cache()
     return {
