@@ -48,7 +48,7 @@ _ENUM_LIMIT = 1 << 22
 
 # counters for the bench / tests: which path each step took
 STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0, "grouped": 0,
-         "k_merged": 0}
+         "k_merged": 0, "folded": 0}
 
 
 # optional per-launch device timing: set TIMING = [] to collect
@@ -247,29 +247,31 @@ def _launch_native(m: Match, leaf, box, out: DeviceTile, ins, stream, accumulate
         c = accs[m.roles["c"]].var_names[0]
         if st["B"][2] != 1 or st["c"][0] != 1:
             return False
-        _native.call("td_ttv", s, ext[a], ext[b], ext[c], _p(v["B"]), st["B"][0], st["B"][1],
-                     _p(v["c"]), _p(o), ost[0], ost[1], accumulate)
+        _timed_call("ttv", stream, "td_ttv", s, ext[a], ext[b], ext[c], _p(v["B"]), st["B"][0], st["B"][1],
+                    _p(v["c"]), _p(o), ost[0], ost[1], accumulate)
     elif m.kind == "ttm":
         a, b, d = leaf.lhs.var_names
         c = accs[m.roles["B"]].var_names[2]
         if st["B"][2] != 1 or st["C"][1] != 1 or ost[2] != 1:
             return False
-        _native.call("td_ttm", s, ext[a], ext[b], ext[c], ext[d], _p(v["B"]), st["B"][0], st["B"][1],
-                     _p(v["C"]), st["C"][0], _p(o), ost[0], ost[1], accumulate)
+        _timed_call("ttm", stream, "td_ttm", s, ext[a], ext[b], ext[c], ext[d], _p(v["B"]), st["B"][0],
+                    st["B"][1], _p(v["C"]), st["C"][0], _p(o), ost[0], ost[1], accumulate)
     elif m.kind == "mttkrp":
         a, b = leaf.lhs.var_names
         _, c, d = accs[m.roles["B"]].var_names
         if st["B"][2] != 1 or st["C"][1] != 1 or st["D"][1] != 1 or ost[1] != 1:
             return False
-        _native.call("td_mttkrp", s, ext[a], ext[c], ext[d], ext[b], _p(v["B"]), st["B"][0], st["B"][1],
-                     _p(v["C"]), st["C"][0], _p(v["D"]), st["D"][0], _p(o), ost[0], accumulate)
+        _timed_call("mttkrp", stream, "td_mttkrp", s, ext[a], ext[c], ext[d], ext[b], _p(v["B"]), st["B"][0],
+                    st["B"][1], _p(v["C"]), st["C"][0], _p(v["D"]), st["D"][0], _p(o), ost[0], accumulate)
     elif m.kind == "innerprod":
         ok = _innerprod(v["B"], v["C"], o, stream, accumulate)
         if not ok:
             return False
     elif m.kind == "contract":
+        ev = _timing_start(stream)
         _contract(leaf.lhs.var_names, accs[m.roles["P"]].var_names, accs[m.roles["Q"]].var_names,
                   o, v["P"], v["Q"], ext, stream, accumulate)
+        _timing_stop("contract", ev, stream)
     else:
         return False
     STATS[m.kind] += 1
@@ -424,8 +426,8 @@ def _innerprod(b: DeviceTile, c: DeviceTile, out: DeviceTile, stream, accumulate
     if rb is None or rc is None or rb[:2] != rc[:2]:
         return False
     work = device_buffer((int(_native.lib().td_innerprod_work_size()),), out.data.device, stream)
-    _native.call("td_innerprod", stream_handle(stream), rb[0], rb[1], _p(b), rb[2], _p(c), rc[2],
-                 _p(out), C.c_void_p(work.data_ptr()), accumulate)
+    _timed_call("innerprod", stream, "td_innerprod", stream_handle(stream), rb[0], rb[1], _p(b), rb[2], _p(c),
+                rc[2], _p(out), C.c_void_p(work.data_ptr()), accumulate)
     if stream is not None:
         work.record_stream(stream)
     return True
@@ -469,8 +471,8 @@ def _dgemm(stream, M, N, K, a, lda, b, ldb, c, ldc, accumulate, keep=()) -> None
     if _GEMM_BATCH is not None and M > 0 and N > 0 and K > 0:
         _GEMM_BATCH.append((stream, accumulate, (M, N, K, a, lda, b, ldb, c, ldc), keep))
         return
-    _native.call("td_dgemm", stream_handle(stream), M, N, K, C.c_void_p(a), lda, C.c_void_p(b), ldb,
-                 C.c_void_p(c), ldc, accumulate)
+    _timed_call("dgemm", stream, "td_dgemm", stream_handle(stream), M, N, K, C.c_void_p(a), lda, C.c_void_p(b),
+                ldb, C.c_void_p(c), ldc, accumulate)
 
 
 def _k_adjacent(first, nxt) -> bool:
@@ -535,6 +537,15 @@ def _launch_group(stream, chunk, acc) -> None:
 
 
 GROUP_MAX = 8
+
+
+def _timed_call(kind, stream, name, *args) -> None:
+    """A leaf's native call, bracketed by CUDA events when TIMING collects
+    them: recorded right around the call, after the host-side preparation,
+    so a GPU idling while Python prepares the launch is not counted."""
+    ev = _timing_start(stream)
+    _native.call(name, *args)
+    _timing_stop(kind, ev, stream)
 
 
 def _timing_start(stream):
@@ -609,10 +620,8 @@ def contracted_var(m, leaf):
 def run_native_box(m, leaf, box, out: DeviceTile, ins, stream, accumulate: int = 1) -> None:
     """Launch the native contraction `m` over `box` (a sub-box of the nest's
     iteration box: the pipelined first step runs its k-range in pieces)."""
-    ev = _timing_start(stream)
     if not _launch_native(m, leaf, box, out, ins, stream, accumulate):
         raise TendistError(f"native {m.kind} leaf cannot address its operands on the box {box}")
-    _timing_stop(m.kind, ev, stream)
 
 
 def _zero_tile(out: DeviceTile, stream) -> None:
@@ -647,9 +656,7 @@ def run_leaf(policy: str, loops, leaf, defs, out: DeviceTile, ins, stream, accum
                 if not zeroed and _sub(out, leaf.lhs, box).rect != out.rect:
                     _zero_tile(out, stream)
                     zeroed, acc = True, 1
-                ev = _timing_start(stream)
                 if _launch_native(m, leaf, box, out, ins, stream, acc):
-                    _timing_stop(m.kind, ev, stream)
                     return m.kind
         if want not in ("auto",):
             raise ConfigError(f"leaf kernel {policy!r} does not apply to {leaf!r} on this nest")
