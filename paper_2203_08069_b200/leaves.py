@@ -48,7 +48,7 @@ _ENUM_LIMIT = 1 << 22
 
 # counters for the bench / tests: which path each step took
 STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0, "grouped": 0,
-         "k_merged": 0, "folded": 0}
+         "k_merged": 0}
 
 
 # optional per-launch device timing: set TIMING = [] to collect
