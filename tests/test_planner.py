@@ -62,3 +62,20 @@ def test_buffer_program_is_consistent(fix):
                 if name != prog.plan.out_name:
                     assert covered == [], (name, rect)
                 assert all(prog.holdings[h].proc == w.task.coord for h in hids)
+
+
+def test_placement_policies_map_processors_to_gpus():
+    """block: contiguous runs of processors per GPU; cyclic: round robin;
+    identity whenever there is a GPU per processor."""
+    from paper_2203_08069_b200 import machine as mach
+    m = td.grid(2, 2, 2)
+    procs = list(m.enumerate())
+    assert [m.device_of(p, 4) for p in procs] == [0, 0, 1, 1, 2, 2, 3, 3]
+    mach.set_placement("cyclic")
+    try:
+        assert [m.device_of(p, 4) for p in procs] == [0, 1, 2, 3, 0, 1, 2, 3]
+        assert [m.device_of(p, 8) for p in procs] == list(range(8))
+    finally:
+        mach.set_placement("block")
+    with pytest.raises(td.ConfigError):
+        mach.set_placement("random")

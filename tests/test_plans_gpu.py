@@ -129,3 +129,47 @@ def test_grouped_gemm_equals_separate_launches():
     torch.cuda.synchronize()
     for c0, c1 in sep:
         assert torch.equal(c0, c1)
+
+
+def test_plan_cache_follows_the_store_and_switches():
+    """A plan is keyed on the program, the output's freshness, the pieces'
+    addresses and the streams: re-placing an input (new buffers) records a
+    new plan; PLANS = False runs the Python loop; a Python plugin is never
+    recorded; all give the oracle's values."""
+    b = BUNDLES["summa"]()
+    ins = td.random_inputs(b.statement, 3)
+    want = seq_eval(td.format_statement(b.statement), b.statement.extents, {k: v.data for k, v in ins.items()})
+    cin = b.scheduled()
+    store, _ = runtime.prepare_store(cin, b.machine, b.distributions, ins)
+
+    def run():
+        store.zero("C")
+        td.execute(cin, store)
+        return store.gather("C").data
+
+    for _ in range(3):
+        assert np.array_equal(run(), want)
+    plans = lambda: [v for v in store.__dict__["_launch_plans"].values() if isinstance(v, tuple)]  # noqa: E731
+    assert len(plans()) == 1
+    ins2 = td.random_inputs(b.statement, 4)
+    store.place("A", ins2["A"], b.distributions["A"])          # new buffers for A
+    want2 = seq_eval(td.format_statement(b.statement), b.statement.extents,
+                     {"A": ins2["A"].data, "B": ins["B"].data})
+    for _ in range(3):
+        assert np.array_equal(run(), want2)
+    assert len(plans()) == 2
+    runtime.PLANS = False
+    try:
+        assert np.array_equal(run(), want2)
+    finally:
+        runtime.PLANS = True
+
+    from oracle.ref_leaf import NAME, innermost_vars, numpy_leaf
+    td.register_leaf_kernel(NAME, numpy_leaf)
+    cin3 = b.schedule.substitute_leaf(innermost_vars(cin), NAME).apply(td.lower_to_cin(b.statement))
+    store3, _ = runtime.prepare_store(cin3, b.machine, b.distributions, ins)
+    for _ in range(3):
+        store3.zero("C")
+        td.execute(cin3, store3)
+        assert np.array_equal(store3.gather("C").data, want)
+    assert not any(isinstance(v, tuple) for v in store3.__dict__.get("_launch_plans", {}).values())
