@@ -41,7 +41,7 @@ def placement() -> str:
 
 
 class Machine:
-    __slots__ = ("levels", "_procs")
+    __slots__ = ("levels", "_procs", "_flat", "_size", "_rank")
 
     def __init__(self, levels):
         lv = tuple(tuple(int(d) for d in level) for level in levels)
@@ -50,8 +50,13 @@ class Machine:
         if any(d <= 0 for level in lv for d in level):
             raise EmptyGrid(f"machine extents must be positive: {lv}")
         object.__setattr__(self, "levels", lv)
-        flat = [d for level in lv for d in level]
-        object.__setattr__(self, "_procs", tuple(itertools.product(*map(range, flat))))
+        flat = tuple(d for level in lv for d in level)
+        procs = tuple(itertools.product(*map(range, flat)))
+        object.__setattr__(self, "_procs", procs)
+        object.__setattr__(self, "_flat", flat)
+        object.__setattr__(self, "_size", reduce(lambda a, b: a * b, flat, 1))
+        # rank lookups sit on every executor step (processor -> GPU): precomputed
+        object.__setattr__(self, "_rank", {p: r for r, p in enumerate(procs)})
 
     def __setattr__(self, name, value):
         raise AttributeError("Machine is immutable")
@@ -70,7 +75,7 @@ class Machine:
 
     @property
     def flat_dims(self) -> tuple:
-        return tuple(d for level in self.levels for d in level)
+        return self._flat
 
     @property
     def num_levels(self) -> int:
@@ -78,15 +83,18 @@ class Machine:
 
     @property
     def size(self) -> int:
-        return reduce(lambda a, b: a * b, self.flat_dims, 1)
+        return self._size
 
     def enumerate(self) -> tuple:
         """Processors in lexicographic order of their flat coordinates."""
         return self._procs
 
     def rank_of(self, coord) -> int:
+        r = self._rank.get(tuple(coord))
+        if r is not None:
+            return r
         r = 0
-        for extent, c in zip(self.flat_dims, coord):
+        for extent, c in zip(self._flat, coord):
             r = r * extent + c
         return r
 

@@ -545,7 +545,11 @@ class _Executor:
         self.credits = {}            # id(inbox) -> plan-owned credit event (while recording)
 
     def gpu(self, p) -> int:
-        return self.m.device_of(p, self.W.ngpus)
+        cache = self.__dict__.setdefault("_gpu_of", {})
+        g = cache.get(p)
+        if g is None:
+            g = cache[p] = self.m.device_of(p, self.W.ngpus)
+        return g
 
     def cstream(self, g):
         return self.W.streams(g)[0]
