@@ -218,6 +218,8 @@ def classify(leaf) -> Match | None:
 def _sub(tile: DeviceTile, acc: Access, box) -> DeviceTile:
     lo = tuple(box[v][0] for v in acc.var_names)
     hi = tuple(box[v][1] for v in acc.var_names)
+    if lo == tile.rect.lo and hi == tile.rect.hi:
+        return tile           # the tile already is the box (the common case): no new view
     return tile.view(HyperRect(lo, hi))
 
 

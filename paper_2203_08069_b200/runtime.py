@@ -96,7 +96,7 @@ def _copy_box(stream, dst, src, accumulate=False):
 
 def _slice(buf, rect: HyperRect, box: HyperRect):
     """View of the part `box` of a buffer that holds `rect`."""
-    if not box.lo:
+    if not box.lo or (box.lo == rect.lo and box.hi == rect.hi):
         return buf
     return buf[tuple(slice(a - o, b - o) for a, b, o in zip(box.lo, box.hi, rect.lo))]
 
