@@ -207,3 +207,16 @@ def test_real_innerprod_1024_within_gamma():
     k = n ** 3
     assert abs(got - want) <= gamma(k + 1) * absum
     assert abs(got - want) <= 1e-10 * k * absum
+
+
+@pytest.mark.parametrize("case", ["gemm", "ttm", "mttkrp", "ttv"])
+def test_real_ragged_large_within_gamma(case):
+    """Large shapes that are not multiples of any tile (TMA zero-filled edges,
+    ragged last blocks of every distributed dimension), multi-task layouts on
+    one GPU, uniform(-1,1) inputs, against the long-double point oracle."""
+    b = {"gemm": lambda: td.summa(2, 2, dims=(4099, 3071, 5003), chunk=1023),
+         "ttm": lambda: td.ttm2d(2, 1, dims=(301, 257, 1021, 61)),
+         "mttkrp": lambda: td.mttkrp(2, 2, dims=(203, 29, 517, 1021)),
+         "ttv": lambda: td.ttv(3, dims=(513, 1027, 2051))}[case]()
+    depth = {"gemm": 1, "ttm": 1, "mttkrp": 2, "ttv": 1}[case]
+    _check_real(b, depth, seed=7)
