@@ -1,10 +1,27 @@
 // Library-level entry points: version, errors, devices, launch counter.
 #include "common.cuh"
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 namespace td {
 static thread_local char t_err[1024] = {0};
 std::atomic<long long> g_launches{0};
+
+// kernels whose dynamic-shared-memory limit was already raised, per device
+static std::mutex g_attr_mu;
+static std::set<std::tuple<const void*, int, int>> g_attr_done;
+
+bool smem_attr_done(const void* kern, int dev, int bytes) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  return g_attr_done.count({kern, dev, bytes}) != 0;
+}
+
+void smem_attr_mark(const void* kern, int dev, int bytes) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  g_attr_done.insert({kern, dev, bytes});
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;

@@ -43,6 +43,22 @@ struct StreamDevice {
   }
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (it is a host round trip; launches of the same kernel repeat it otherwise).
+bool smem_attr_done(const void* kern, int dev, int bytes);   // capi.cu
+void smem_attr_mark(const void* kern, int dev, int bytes);
+
+template <class Kernel>
+inline cudaError_t ensure_smem(Kernel kern, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorUnknown;
+  const void* key = reinterpret_cast<const void*>(kern);
+  if (smem_attr_done(key, dev, bytes)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) smem_attr_mark(key, dev, bytes);
+  return e;
+}
+
 inline int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();

@@ -312,7 +312,7 @@ static int launch_gemm(cudaStream_t st, int64_t batch, GemmArgs a) {
   auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, VEC, KP, EPI>;
   static bool configured = false;  // attribute is per-device; cheap to re-set
   (void)configured;
-  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  TD_CUDA(ensure_smem(kern, Cfg::SMEM_BYTES));
   a.tiles_m = (int)ceil_div(a.M, BM);
   a.tiles_n = (int)ceil_div(a.N, BN);
   a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);

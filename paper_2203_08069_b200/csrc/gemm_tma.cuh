@@ -16,6 +16,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+#include <unordered_map>
+
 namespace td {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -293,9 +296,52 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   return fn;
 }
 
-// k4-sliced 4-D view {4, rows, cols/4, batch} of a row-major [batch][rows][cols] operand
+// k4-sliced 4-D view {4, rows, cols/4, batch} of a row-major [batch][rows][cols] operand.
+// Encoded maps are cached by their parameters (repeated launches on the same
+// tiles -- every step of a launch plan -- skip the driver call).
+static int encode_sliced_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                             int64_t batch, int64_t batch_stride, int box_rows, int box_cols);
+
+struct MapKey {
+  const double* base;
+  int64_t rows, cols, ld, batch, stride;
+  int box_rows, box_cols;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && batch == o.batch &&
+           stride == o.stride && box_rows == o.box_rows && box_cols == o.box_cols;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.base);
+    for (int64_t v : {k.rows, k.cols, k.ld, k.batch, k.stride, int64_t(k.box_rows) << 32 | k.box_cols})
+      h = (h ^ uint64_t(v)) * 0x9E3779B97F4A7C15ull;
+    return size_t(h ^ (h >> 29));
+  }
+};
+
 static int make_sliced_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
                            int64_t batch, int64_t batch_stride, int box_rows, int box_cols) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{base, rows, cols, ld, batch, batch > 1 ? batch_stride : 0, box_rows, box_cols};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *map = it->second;
+      return TD_OK;
+    }
+  }
+  if (int rc = encode_sliced_map(map, base, rows, cols, ld, batch, batch_stride, box_rows, box_cols)) return rc;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() > 8192) cache.clear();
+  cache.emplace(key, *map);
+  return TD_OK;
+}
+
+static int encode_sliced_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                             int64_t batch, int64_t batch_stride, int box_rows, int box_cols) {
   auto enc = tma_encoder();
   TD_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled is unavailable");
   const cuuint64_t dims[4] = {4, (cuuint64_t)rows, (cuuint64_t)(cols / 4), (cuuint64_t)batch};
@@ -320,7 +366,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB 
 static int launch_gemm_tma(cudaStream_t st, int64_t batch, GemmArgs a) {
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, STAGES, EPI, MINB>;
-  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  TD_CUDA(ensure_smem(kern, Cfg::SMEM_BYTES));
   CUtensorMap ma, mb;
   if (int rc = make_sliced_map(&ma, a.A, a.M, a.K, a.lda, batch, a.sA, BM, BK)) return rc;
   if (int rc = make_sliced_map(&mb, a.B, a.K, a.N, a.ldb, a.sB ? batch : 1, a.sB, BK, BN)) return rc;
@@ -344,7 +390,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
 static int launch_gemm_tma_grouped(cudaStream_t st, int count, const GemmArgs* probs) {
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   auto kern = dgemm_tma_grouped_kernel<BM, BN, BK, WM, WN, STAGES, MINB>;
-  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  TD_CUDA(ensure_smem(kern, Cfg::SMEM_BYTES));
   GroupedTma g;
   std::memset(&g, 0, sizeof g);
   g.count = count;

@@ -178,7 +178,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
 static int launch_gemm_ws(cudaStream_t st, int64_t batch, GemmArgs a) {
   using W = WsCfg<BM, BN, BK, WM, WN, STAGES>;
   auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, VEC>;
-  TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, W::SMEM_BYTES));
+  TD_CUDA(ensure_smem(kern, W::SMEM_BYTES));
   a.tiles_m = (int)ceil_div(a.M, BM);
   a.tiles_n = (int)ceil_div(a.N, BN);
   a.group = raster_group(1, BM, BN);

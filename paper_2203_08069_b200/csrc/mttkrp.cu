@@ -288,11 +288,11 @@ static int launch_mttkrp(cudaStream_t st, MttkrpArgs a, bool vec2) {
     dim3 grid((unsigned)(a.I * a.groups), (unsigned)ceil_div(a.R, MK_R));
     if (vec2) {
       auto kern = mttkrp_kernel<WARPS, STAGES, KPC, BK, CSMEM, MINB, 2>;
-      TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      TD_CUDA(ensure_smem(kern, Cfg::SMEM));
       kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
     } else {
       auto kern = mttkrp_kernel<WARPS, STAGES, KPC, BK, CSMEM, MINB, 1>;
-      TD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+      TD_CUDA(ensure_smem(kern, Cfg::SMEM));
       kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
     }
     if (int rc = check_launch("mttkrp_kernel")) return rc;
