@@ -505,6 +505,29 @@ def _leaf_choice(relations, loop_vars, policy):
     return policy, None
 
 
+# NVTX ranges around each step's transfers / leaves and the commit phase
+# (TD_NVTX=1): host-side ranges a profiler (ncu --nvtx, nsys) attributes the
+# launches to; off by default (they cost a few microseconds each)
+NVTX = os.environ.get("TD_NVTX", "0") == "1"
+
+
+class _nvtx:
+    __slots__ = ("name",)
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if NVTX:
+            torch_mod().cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if NVTX:
+            torch_mod().cuda.nvtx.range_pop()
+        return False
+
+
 class _NoBatch:
     def __enter__(self):
         return self
@@ -649,7 +672,8 @@ class _Executor:
                 self._steps(nsteps)
             if not self.prog.stepwise:
                 self.compute(self.prog.work[-1], -1)
-            self.commit(out_region)
+            with _nvtx("commit"):
+                self.commit(out_region)
             self._mark_done(out_region, self.prog.commits)
         for g in self.owned:
             cur = torch.cuda.current_stream(self.W.device(g))
@@ -663,22 +687,25 @@ class _Executor:
                                       for a in accesses_of(leaf.rhs)}
 
     def _steps(self, nsteps):
-        if True:
-            for s in range(nsteps):
-                if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
-                    for g in self.owned:
-                        self._sync(self.xstream(g), self.cstream(g))
-                split = self._split_plan(s) if s == 0 and self.prog.stepwise else None
-                if split is not None:
-                    self.compute_split(self.prog.work[s], s, split, self.transfers_split(self.prog.transfers[s], split))
-                    self.release(s)
-                    continue
-                self.transfers(self.prog.transfers[s])
+        for s in range(nsteps):
+            if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
                 for g in self.owned:
-                    self._sync(self.cstream(g), self.xstream(g))
-                if self.prog.stepwise:
-                    self.compute(self.prog.work[s], s)
+                    self._sync(self.xstream(g), self.cstream(g))
+            split = self._split_plan(s) if s == 0 and self.prog.stepwise else None
+            if split is not None:
+                with _nvtx(f"step {s} pipelined"):
+                    self.compute_split(self.prog.work[s], s, split,
+                                       self.transfers_split(self.prog.transfers[s], split))
                 self.release(s)
+                continue
+            with _nvtx(f"step {s} transfers"):
+                self.transfers(self.prog.transfers[s])
+            for g in self.owned:
+                self._sync(self.cstream(g), self.xstream(g))
+            if self.prog.stepwise:
+                with _nvtx(f"step {s} leaves"):
+                    self.compute(self.prog.work[s], s)
+            self.release(s)
 
     def _inboxes(self) -> dict:
         """{task coord: peer.Inbox} of the write-backs that go through peer
