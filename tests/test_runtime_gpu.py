@@ -268,3 +268,14 @@ def test_place_file_rejects_wrong_payload_size(tmp_path):
             store.place_file("A", p, b.distributions["A"])
     store.place_file("A", good, b.distributions["A"])
     assert store["A"].tensor == t
+
+
+def test_nvtx_ranges_do_not_change_results():
+    from paper_2203_08069_b200 import runtime
+    b = td.cannon(2, 2, dims=(40, 36, 44))
+    runtime.NVTX = True
+    try:
+        res, ins = b.run(seed=2)
+    finally:
+        runtime.NVTX = False
+    assert np.array_equal(res.output.data, ins["A"].data @ ins["B"].data)
