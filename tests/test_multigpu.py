@@ -125,3 +125,13 @@ print("abi collectives OK")
 """ % ROOT
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "abi collectives OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_reference_suite_under_spmd():
+    """The reference's own unit tests with every launch spread over 2 GPUs (tests/ref_suite_spmd.py)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+           "--master-port", "29543", os.path.join(ROOT, "tests", "ref_suite_spmd.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ref_suite_spmd world=2" in out.stdout and "OK" in out.stdout, \
+        out.stdout[-3000:] + out.stderr[-3000:]
