@@ -38,8 +38,8 @@ class CommEvent:
     tensor: str
     rect: HyperRect
     elements: int
-    kind: str    # "copy" | "reduce"
-    phase: str   # "compute" | "placement"
+    kind: str    # copy (fetch / write-back) or reduce (accumulated into the home)
+    phase: str   # compute (inside a launch) or placement (redistribute)
 
 
 @_record
@@ -58,7 +58,7 @@ class Requirement:
     step: int
     tensor: str
     rect: HyperRect
-    scope: str   # "launch" | "step"
+    scope: str   # fetched once per launch, or again every step
 
 
 def _rollup(events, key=None) -> dict:
@@ -84,9 +84,8 @@ class ExecutionTrace:
 
     def __init__(self, machine: Machine):
         self.machine = machine
-        self.events: list = []
-        self.launches: list = []
-        self.requirements: list = []
+        # the ledger: transfers, launch records, per-task needs (debug)
+        self.events, self.launches, self.requirements = [], [], []
         self.num_steps = 0
         self.memory = dict.fromkeys(machine.enumerate(), 0)
         self.timings: list = []
@@ -105,7 +104,8 @@ class ExecutionTrace:
     # -- queries ----------------------------------------------------------------
     @property
     def high_water(self) -> int:
-        return max(self.memory.values(), default=0)
+        """Largest per-processor resident element count."""
+        return max([0, *self.memory.values()])
 
     def events_of(self, kind=None, phase=None, tensor=None, step=None) -> list:
         wanted = [(_FILTER_FIELDS[k], v) for k, v in
@@ -114,11 +114,11 @@ class ExecutionTrace:
 
     @property
     def total_messages(self) -> int:
-        return len(self.events)
+        return _pair(_rollup(self.events).get(None))["messages"]
 
     @property
     def total_elements(self) -> int:
-        return sum(e.elements for e in self.events)
+        return _pair(_rollup(self.events).get(None))["elements"]
 
     def per_edge(self) -> list:
         groups = _rollup(self.events, key=lambda e: (e.src, e.dst))
@@ -185,7 +185,8 @@ class ExecutionTrace:
 
 
 def write_edge_csv(trace: ExecutionTrace, path) -> None:
-    """Per-edge aggregate as CSV: src,dst,messages,elements."""
+    """The per_edge table as CSV (header src,dst,messages,elements; grid
+    coordinates joined with "x")."""
     rows = [["src", "dst", "messages", "elements"]]
     rows += [["x".join(map(str, r["src"])), "x".join(map(str, r["dst"])), r["messages"], r["elements"]]
              for r in trace.per_edge()]
