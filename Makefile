@@ -24,7 +24,13 @@ LIB       := $(PKG)/libdistal_b200.so
 REF_PKG   ?= /root/reference/pkg
 REF_OUT   := oracle/_ref
 
-all: $(LIB) ref
+all: $(LIB) ref examples
+
+# a C host using only the C ABI (td_execute_plan); tests/test_abi_host.py runs it on a GPU
+examples: examples/plan_demo
+
+examples/plan_demo: examples/plan_demo.c include/distal_b200.h $(LIB)
+	$(NVCC) -x cu $(ARCH) -O2 -Iinclude $< -o $@ -L$(PKG) -ldistal_b200 -Xlinker -rpath -Xlinker '$$ORIGIN/../$(PKG)'
 
 ref:
 	@if [ -d $(REF_PKG)/src/tendist ]; then \
@@ -42,6 +48,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) $(LDFLAGS) $(OBJS) -o $@
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) examples/plan_demo
 
-.PHONY: all clean ref
+.PHONY: all clean ref examples
