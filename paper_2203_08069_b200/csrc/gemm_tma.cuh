@@ -30,6 +30,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done;
@@ -177,6 +181,7 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   extern __shared__ __align__(128) unsigned char tma_smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];   // per stage: every warp has read it
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 127) & ~uintptr_t(127));
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
@@ -205,7 +210,10 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
 
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::THREADS / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -234,8 +242,13 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
 
   for (int kt = 0; kt < ktiles; ++kt) {
     mbar_wait(&full[kt % STAGES], (kt / STAGES) & 1);
-    __syncthreads();  // every warp is done with the stage the next copy overwrites
-    if (tid == 0 && kt + STAGES - 1 < ktiles) issue(kt + STAGES - 1);
+    if (tid == 0 && kt + STAGES - 1 < ktiles) {
+      // the slot the next copy overwrites was read in iteration kt - 1: wait until every
+      // warp released it (per-stage "empty" barrier instead of a CTA-wide __syncthreads,
+      // so the other warps never wait for each other)
+      if (kt >= 1) mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
+      issue(kt + STAGES - 1);
+    }
     const double* as = As + (kt % STAGES) * Cfg::A_STAGE + a_off;
     const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE + b_off;
 #pragma unroll
@@ -250,6 +263,8 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
 #pragma unroll
         for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[kt % STAGES]);
   }
 
   if constexpr (EPI == 1) __syncthreads();  // every stage has been consumed: the ring serves as scratch
