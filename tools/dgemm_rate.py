@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 from paper_2203_08069_b200 import _native as nat  # noqa: E402
 
-nat.load()
+nat.load(os.environ.get("TD_LIB", nat.LIB_PATH))
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 a = torch.rand(n, n, dtype=torch.float64, device="cuda")
 b = torch.rand(n, n, dtype=torch.float64, device="cuda")
