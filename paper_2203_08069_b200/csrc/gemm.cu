@@ -424,7 +424,9 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // (atomic counter, claim latency hidden one tile ahead, the ring running
 // across tile boundaries, both EPI forms) measured 33.8 (MTTKRP) and 35.8
 // (TTM) against 35.0 / 36.1 here: co-resident CTAs already hide a new
-// tile's cold pipeline, so the per-tile CTAs stay.
+// tile's cold pipeline, so the per-tile CTAs stay.  With the per-stage empty
+// barriers, deeper rings for MTTKRP (tools/mttkrp_configs.py): 128x32x8 with 6
+// stages / 3 CTAs 34.45, 128x32x16 with 4 stages / 2 CTAs 32.07, vs 34.95.
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;
