@@ -112,6 +112,21 @@ class Region:
         self.residency = dist.residency()
         self.pieces = {}          # (gpu, color) -> CUDA tensor holding piece_bounds(color)
         self.zeroed = False       # every piece is known to hold +0.0 (fresh output)
+        # pieces that are +0.0 by contract but not yet in memory (RegionStore.zero is lazy:
+        # the first leaf writing a whole piece overwrites it; anything else fills it first)
+        self.pending_zero = set()
+
+    def materialize(self) -> None:
+        """Write the zeros `RegionStore.zero` deferred (before any read)."""
+        if not self.pending_zero:
+            return
+        torch = torch_mod()
+        for key in sorted(self.pending_zero, key=repr):
+            buf = self.pieces.get(key)
+            if buf is not None:
+                _native.call("td_fill", stream_handle(torch.cuda.current_stream(buf.device)),
+                             C.c_void_p(buf.data_ptr()), buf.numel(), 0.0)
+        self.pending_zero = set()
 
     @property
     def store(self):
@@ -352,10 +367,16 @@ class RegionStore:
                 stream.wait_event(ev)
 
     def zero(self, name: str) -> None:
-        """Reset every resident piece of a region to +0.0 (a fresh output)."""
-        for buf in self.regions[name].pieces.values():
-            buf.zero_()
-        self.regions[name].zeroed = True
+        """Reset every resident piece of a region to +0.0 (a fresh output).
+
+        Lazy: the pieces are only marked.  The next launch writing the region
+        lets the first leaf of each task that owns a whole piece overwrite it
+        (0 + x = x: the same bits as accumulating into zeros, without the fill
+        pass or the epilogue's read of the old values) and fills the rest;
+        every read path (gather, local_pieces, redistribute, ...) fills first."""
+        region = self.regions[name]
+        region.pending_zero = set(region.pieces)
+        region.zeroed = True
 
     def place_generated(self, name: str, dist: TensorDistribution, *, seed=0, tensor_id=0,
                         mode=0) -> Region:
@@ -383,6 +404,7 @@ class RegionStore:
         instead of hanging.  Use `local_pieces` for rank-local reads."""
         torch = torch_mod()
         region = self.regions[name]
+        region.materialize()
         out = np.zeros(region.dims, dtype=np.float64)
         W = self.world
         if W.multi_gpu:
@@ -410,6 +432,7 @@ class RegionStore:
     def local_pieces(self, name: str):
         """(box, CUDA tensor) for the home pieces of `name` on this process's GPUs."""
         region = self.regions[name]
+        region.materialize()
         for color, box, procs in region.dist.pieces():
             gpus = region.gpus_of(color)
             if gpus and self.world.owns(gpus[0]):
@@ -640,6 +663,7 @@ class _Executor:
         self.store.row_done = {k: v for k, v in self.store.row_done.items() if k[0] != self.plan.out_name}
         self.direct = self._direct_commits(out_region)
         self.inbox = self._inboxes()
+        self.overwrite = self._lazy_zeros(out_region)
         for t in self.plan.tasks:
             g = self.gpu(t.coord)
             if t.out_rect is not None and self.W.owns(g):
@@ -672,6 +696,7 @@ class _Executor:
                 self._steps(nsteps)
             if not self.prog.stepwise:
                 self.compute(self.prog.work[-1], -1)
+            self._fill_unwritten()
             with _nvtx("commit"):
                 self.commit(out_region)
             self._mark_done(out_region, self.prog.commits)
@@ -681,6 +706,56 @@ class _Executor:
             self._sync(cur, self.xstream(g))
         self.buffers.clear()
         self.out_bufs.clear()
+
+    def _lazy_zeros(self, out_region) -> set:
+        """Resolve `RegionStore.zero`'s deferred zeros for this launch: the
+        tasks writing a whole pending output piece directly get their first
+        leaf as an overwrite (returned); every other pending piece, of the
+        output or of any region the launch reads, is filled now."""
+        overwrite = set()
+        task_loops, _ = _loops_of(self.plan.task_body)
+        _, plugins = _leaf_choice(self.plan.relations, [v for v, _, _ in task_loops], self.policy)
+        if out_region.pending_zero and not plugins and not self._reads_output():
+            for t in self.plan.tasks:
+                color = self.direct.get(t.coord)
+                key = (self.gpu(t.coord), color)
+                if color is not None and key in out_region.pending_zero:
+                    overwrite.add(t.coord)
+                    out_region.pending_zero.discard(key)
+        for region in self.store.regions.values():
+            if not region.pending_zero:
+                continue
+            for key in sorted(region.pending_zero, key=repr):
+                g = key[0]
+                if self.W.owns(g) and key in region.pieces:
+                    buf = region.pieces[key]
+                    _native.call("td_fill", stream_handle(self.cstream(g)), C.c_void_p(buf.data_ptr()),
+                                 buf.numel(), 0.0)
+            region.pending_zero = set()
+        return overwrite
+
+    def _fill_unwritten(self, coords=None) -> None:
+        """A task granted the first-leaf overwrite that ran no leaf at all
+        (no iteration points) still owes its piece the zeros."""
+        for coord in sorted(self.overwrite if coords is None else self.overwrite & set(coords)):
+            self.overwrite.discard(coord)
+            buf = self.out_bufs.get(coord)
+            if buf is not None:
+                from .leaves import flush_pending
+                flush_pending()
+                _native.call("td_fill", stream_handle(self.cstream(self.gpu(coord))), C.c_void_p(buf.data_ptr()),
+                             buf.numel(), 0.0)
+
+    def _acc_of(self, coord) -> int:
+        """0: this task's leaf overwrites its output tile (a peer inbox, or the
+        first leaf into a lazily zeroed piece; run_leaf zero-fills when the
+        leaf does not cover the tile), else 1 (accumulate)."""
+        if coord in self.inbox:
+            return 0
+        if coord in self.overwrite:
+            self.overwrite.discard(coord)
+            return 0
+        return 1
 
     def _reads_output(self) -> bool:
         return self.plan.out_name in {a.tensor.name for leaf in leaf_statements(self.plan.task_body)
@@ -755,6 +830,7 @@ class _Executor:
         for task in self.plan.tasks:
             for s, w in by_task.get(task.coord, []):
                 self.compute([w], s)
+            self._fill_unwritten([task.coord])
             mine = commits.get(task.coord, [])
             self._apply_commits(region, [(c, None) for c in mine])
             self._mark_done(region, mine, upto=task.coord)
@@ -1055,7 +1131,7 @@ class _Executor:
                 continue
             st = self.cstream(g)
             self._after(st, events[g][0])
-            acc = 0 if w.task.coord in self.inbox else 1
+            acc = self._acc_of(w.task.coord)
             if any(rect is None for _, rect, _ in w.operands.values()):
                 if not acc:   # an empty access: the partial is all zeros
                     _native.call("td_fill", stream_handle(st), C.c_void_p(self.out_bufs[w.task.coord].data_ptr()),
@@ -1113,7 +1189,7 @@ class _Executor:
             if not self.W.owns(g) or w.task.out_rect is None:
                 continue
             st = self.cstream(g)
-            acc = 0 if w.task.coord in self.inbox else 1     # an inbox is overwritten, not zeroed
+            acc = self._acc_of(w.task.coord)
             if any(rect is None for _, rect, _ in w.operands.values()):
                 if not acc:   # some access is empty on this step: the partial is all zeros
                     _native.call("td_fill", stream_handle(st), C.c_void_p(self.out_bufs[w.task.coord].data_ptr()),
@@ -1430,7 +1506,8 @@ def _plan_key(prog, store, policy):
     out = store[prog.plan.out_name]
     pieces = tuple((n, tuple((k, b.data_ptr()) for k, b in r.pieces.items())) for n, r in store.regions.items())
     streams = tuple(torch.cuda.current_stream(W.device(g)).cuda_stream for g in W.owned)
-    return (id(prog), policy, out.zeroed, pieces, streams)
+    pending = tuple(bool(r.pending_zero) for r in store.regions.values())
+    return (id(prog), policy, out.zeroed, pending, pieces, streams)
 
 
 def _launch(prog, store, policy) -> None:
@@ -1478,6 +1555,8 @@ def _replay(plan, prog, store) -> None:
         if ib.credit is not None and not isinstance(ib.credit, _NativeEvent):
             W.streams(ib.writer_gpu)[0].wait_event(ib.credit)
     plan.run()
+    for region in store.regions.values():    # the plan's fills / overwrites resolved them, as when recorded
+        region.pending_zero = set()
     for ib, h in plan.extra["credits"]:
         ib.credit = _NativeEvent(h)
     out = prog.plan.out_name
@@ -1529,6 +1608,7 @@ class CapturedLaunch:
                 if reset_output:
                     for buf in store[self.out].pieces.values():
                         buf.zero_()
+                    store[self.out].pending_zero = set()
                 store[self.out].zeroed = reset_output
                 execute(stmt, store, record_requirements=False, leaf_policy=leaf_policy)
         finally:
@@ -1640,6 +1720,7 @@ def redistribute(store: RegionStore, name: str, new_dist: TensorDistribution,
     moves over NCCL (or stays in place on a shared GPU)."""
     torch = torch_mod()
     region = store.regions[name]
+    region.materialize()
     check_redistributable(region.dist, new_dist)
     old = region.residency
     new = new_dist.residency()
