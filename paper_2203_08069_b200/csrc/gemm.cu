@@ -328,6 +328,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace td
 #include "gemm_tma.cuh"
+#include "mttkrp_tma.cuh"
 #ifdef TD_TUNING
 #include "gemm_ws.cuh"
 #endif
@@ -401,7 +402,8 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
   X(44, 64, 128, 16, 32, 64, 3, 0)             \
   X(47, 64, 64, 16, 32, 32, 3, 4)              \
   X(48, 128, 32, 16, 32, 32, 3, 4)             \
-  X(50, 128, 64, 16, 64, 32, 4, 0)
+  X(50, 128, 64, 16, 64, 32, 4, 0)             \
+  X(51, 256, 32, 16, 32, 32, 3, 2)
 
 // Tile history on B200 (tools/tuning/tune2.py, tune_n32.py, tune_n64.py; 16384^3
 // unless noted):

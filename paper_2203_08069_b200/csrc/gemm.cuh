@@ -36,4 +36,22 @@ int dgemm_rowsum(cudaStream_t st, int config, int64_t batch, GemmArgs a);
 // Does `config` take the TMA body (whose epilogue can finish the sum itself)?
 bool dgemm_rowsum_fusable(int config, int64_t batch, const GemmArgs& a);
 
+// Stream-K MTTKRP (mttkrp_tma.cuh): A(i, j) (+)= sum_(k,l) B(i, k, l) * C(k, j) * D(l, j)
+struct MkSplitArgs {
+  int64_t I, K, L, R;
+  const double* B;
+  int64_t sBi, sBk;
+  const double* C;
+  int64_t ldc;
+  const double* D;
+  int64_t ldd;
+  double* A;
+  int64_t lda;
+  int accumulate;
+};
+// Workspace doubles the variant needs for this shape and its CTA count, or 0
+// when the copy engine cannot address the operands (per-i kernel instead).
+int64_t mttkrp_streamk_plan(int variant, const MkSplitArgs& a, int* ctas);
+int mttkrp_streamk(cudaStream_t st, int variant, const MkSplitArgs& a, int ctas, double* work);
+
 }  // namespace td

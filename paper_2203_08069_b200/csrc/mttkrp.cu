@@ -20,12 +20,14 @@
 // bytes in flight per SM: the configurations trade l-tile depth (BK), stages
 // and resident CTAs per SM (MINB) against shared memory.
 //
-// The default (config 18) runs the same algorithm on the tuned GEMM body
-// instead: a batched GEMM over i, M = k rows, N = j, K = l, whose epilogue
-// (gemm.cu / gemm_tma.cuh, EPI = 1) does the Hadamard with C and the
-// fixed-order sum over the tile's k rows into the same [I][groups][R]
-// workspace; mttkrp_reduce finishes.  Measured 34.8 (TMA-fed body) and 33.4
-// (LDGSTS body) vs 30.9 TFLOP/s for the best fused configuration.
+// The defaults run the same algorithm on the tuned GEMM body instead: a
+// batched GEMM over i, M = k rows, N = j, K = l, whose epilogue (gemm.cu /
+// gemm_tma.cuh, EPI = 1) does the Hadamard with C and the fixed-order sum over
+// the tile's k rows; large shapes take whole-item CTAs plus a stream-K last
+// wave (mttkrp_tma.cuh, config 22), smaller ones the per-i kernel on 256- or
+// 128-row tiles (19 / 18) -- see default_mttkrp_config.  Round 1 measured
+// 34.8 (TMA-fed body) and 33.4 (LDGSTS body) vs 30.9 TFLOP/s for the best
+// fused configuration.
 #include <algorithm>
 #include <map>
 #include <mutex>
@@ -383,17 +385,51 @@ static int launch_mttkrp_gemm(cudaStream_t st, MttkrpArgs a, int gemm_config) {
   return rc;
 }
 
+// Stream-K MTTKRP (gemm.cu / mttkrp_tma.cuh); `required` = false lets shapes
+// the plan rejects fall back to the per-i GEMM body.
+static int launch_mttkrp_streamk(cudaStream_t st, const MttkrpArgs& a, int variant, bool required) {
+  const MkSplitArgs s{a.I, a.K, a.L, a.R, a.B, a.sBi, a.sBk, a.C, a.ldc, a.D, a.ldd, a.A, a.lda, a.accumulate};
+  int ctas = 0;
+  const int64_t words = mttkrp_streamk_plan(variant, s, &ctas);
+  if (words == 0) {
+    TD_REQUIRE(!required, "mttkrp: stream-K variant %d cannot take this shape", variant);
+    return launch_mttkrp_gemm(st, a, 51);
+  }
+  double* work = nullptr;
+  int* counters = nullptr;
+  if (int rc = mk_scratch(st, sizeof(double) * words, sizeof(int), &work, &counters)) return rc;
+  return mttkrp_streamk(st, variant, s, ctas, work);
+}
+
 // configurations 0-7: the fused kernel above, <WARPS, STAGES, k-blocks per CTA,
 // l per stage, C in smem, CTAs per SM>; 8-13, 15, 18: the GEMM body with the
 // row-sum epilogue on GEMM tile configs 26, 29, 21, 20, 34, 35, 43, 48 (the
 // last two TMA-fed)
+// Default by the number of 256-row items per wave of resident CTAs (2 per SM),
+// measured at K = L = 1024, R = 32 (tools/mttkrp_clocks.py, TFLOP/s):
+//   I      waves | 18 (128-row, 3/SM) | 19 (256-row, 2/SM) | 22 (DP + stream-K)
+//   1024   13.8  | 34.95              | 35.29              | 35.42
+//   256     3.5  | 33.59              | 34.41              | 33.84
+//   128     1.7  | 32.23              | 29.56              | 32.05
+//   4096   55    | 35.53              | 35.81              | --
+// Round-1 baseline (the per-i kernel, fused kernel configs 0-7 and the LDGSTS
+// bodies): 34.8 / 30.9 / 33.4.
+static int default_mttkrp_config(const MttkrpArgs& a) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = a.I * ceil_div(std::max<int64_t>(a.K, 1), 256) * ceil_div(a.R, 32);
+  const int64_t waves = items / (2 * int64_t(sms));
+  if (waves >= 8) return 22;
+  if (waves >= 3) return 19;
+  return 18;
+}
+
 int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
   const bool vec2 = al16(a.B) && al16(a.D) && a.sBi % 2 == 0 && a.sBk % 2 == 0 && a.ldd % 2 == 0;
-  // default 18: the TMA-fed GEMM body on 128x32x16 tiles, 3 stages, <= 128
-  // registers -> 34.8 TFLOP/s at 1024^3 r32 (LDGSTS body, config 12: 33.4; fused
-  // kernel, best config 6: 30.9; tools/tuning/tune_n32.py).  Operands the copy
-  // engine cannot address take the LDGSTS body with the same tile.
-  switch (config < 0 ? 18 : config) {
+  // 18 / 19: the TMA-fed GEMM body (128- / 256-row tiles, 16-wide l-tiles, 3
+  // stages); 22: whole-item CTAs plus a stream-K last wave (mttkrp_tma.cuh).
+  // Operands the copy engine cannot address take the LDGSTS body.
+  switch (config < 0 ? default_mttkrp_config(a) : config) {
     case 0: return launch_mttkrp<4, 4, 1, 16, false, 2>(st, a, vec2);
     case 1: return launch_mttkrp<4, 3, 1, 16, true, 2>(st, a, vec2);
     case 2: return launch_mttkrp<4, 3, 2, 16, false, 2>(st, a, vec2);
@@ -410,6 +446,8 @@ int mttkrp_dispatch(cudaStream_t st, const MttkrpArgs& a, int config) {
     case 13: return launch_mttkrp_gemm(st, a, 35);
     case 15: return launch_mttkrp_gemm(st, a, 43);
     case 18: return launch_mttkrp_gemm(st, a, 48);
+    case 19: return launch_mttkrp_gemm(st, a, 51);
+    case 22: return launch_mttkrp_streamk(st, a, 0, config >= 0);
     default:
       set_error("mttkrp: unknown config %d", config);
       return TD_ERR_ARG;

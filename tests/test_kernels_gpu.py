@@ -154,15 +154,18 @@ def test_mttkrp_exact(nat, i, k, l, r, accumulate):
     assert np.array_equal(ta.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("config", list(range(14)) + [15, 18])
+@pytest.mark.parametrize("config", list(range(14)) + [15, 18, 19, 22])
 @pytest.mark.parametrize("i,k,l,r,pad", [(3, 200, 17, 45, 0), (2, 129, 40, 32, 1), (70000, 2, 3, 2, 0),
                                          (3, 130, 44, 36, 0), (70000, 3, 4, 4, 0)])
 def test_mttkrp_every_config(nat, config, i, k, l, r, pad):
-    """Fused kernels (0-7) and the GEMM-body row-sum variants (8-13, 15, 18; 15
-    and 18 fed by TMA): ragged k / l / r tiles, odd strides (scalar cp.async path), shapes
-    the copy engine can address (l, r multiples of 4) and > 65535 batches."""
+    """Fused kernels (0-7) and the GEMM-body row-sum variants (8-13, 15, 18, 19;
+    15, 18 and 19 fed by TMA), whole-item + stream-K (22): ragged k / l / r tiles,
+    odd strides (scalar cp.async path), shapes the copy engine can address (l, r
+    multiples of 4) and > 65535 batches."""
     if i > 1000 and config < 8:
         pytest.skip("the fused kernels have no batch limit to exercise")
+    if config == 22 and (l % 4 or r % 4 or pad % 2):
+        pytest.skip("config 22 is TMA-only (the default falls back to the per-i kernel)")
     rng = np.random.default_rng(config + i + k)
     b, cm, d = ints(rng, i, k, l + pad), ints(rng, k, r), ints(rng, l + pad, r)
     tb, tcm, td = dev(b), dev(cm), dev(d)
@@ -170,6 +173,24 @@ def test_mttkrp_every_config(nat, config, i, k, l, r, pad):
     nat.call("td_mttkrp_config", stream(), config, i, k, l, r, ptr(tb), k * (l + pad), l + pad, ptr(tcm), r,
              ptr(td), r, ptr(ta), r, 1)
     want = 7.0 + ref.mttkrp(b[:, :, :l], cm, d[:l])
+    assert np.array_equal(ta.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("config", [-1, 19, 22])
+@pytest.mark.parametrize("i,k,l,r", [(2000, 256, 64, 32), (600, 300, 100, 36), (10, 256, 1024, 32),
+                                     (1, 1000, 2048, 32), (300, 513, 36, 64), (4800, 256, 16, 32)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_mttkrp_streamk_exact(nat, config, i, k, l, r, accumulate):
+    """Whole-item CTAs + stream-K last wave (config 22): items cut across many
+    sk CTAs (I = 1, 10: no whole-item blocks), tail items cut once or twice,
+    ragged k rows / l tiles, two column tiles (R = 36, 64), exact on integers;
+    the default selection (-1) and the per-i 256-row kernel (19) on the same."""
+    rng = np.random.default_rng(i + k + l + r + accumulate)
+    b, cm, d, a0 = ints(rng, i, k, l), ints(rng, k, r), ints(rng, l, r), ints(rng, i, r)
+    tb, tcm, td, ta = dev(b), dev(cm), dev(d), dev(a0)
+    nat.call("td_mttkrp_config", stream(), config, i, k, l, r, ptr(tb), k * l, l, ptr(tcm), r, ptr(td), r,
+             ptr(ta), r, accumulate)
+    want = ref.mttkrp(b, cm, d) + (a0 if accumulate else 0)
     assert np.array_equal(ta.cpu().numpy(), want)
 
 
