@@ -429,6 +429,13 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 // tile's cold pipeline, so the per-tile CTAs stay.  With the per-stage empty
 // barriers, deeper rings for MTTKRP (tools/mttkrp_configs.py): 128x32x8 with 6
 // stages / 3 CTAs 34.45, 128x32x16 with 4 stages / 2 CTAs 32.07, vs 34.95.
+// Also not kept (tools/ab_kernels.py, A/B builds on one box): refilling a
+// slot from the LAST warp to release it (shared-memory arrival counter, no
+// producer wait, all STAGES slots in flight) -- DGEMM 36.0 vs 36.38, TTM 35.7
+// vs 36.05, MTTKRP 256-row 34.97 vs 35.29; and an L2 prefetch
+// (cp.async.bulk.prefetch.tensor) of the A panel 2-16 k-tiles beyond the ring
+// -- MTTKRP 27.5 vs 35.3 (even an idle prefetch cursor on the issuing thread
+// cost the stream-K kernel 35.42 -> 34.62: the issue path is latency-critical).
 static int default_config(int64_t N) {
   if (N <= 32) return 34;
   return 20;
