@@ -412,6 +412,9 @@ static int launch_mttkrp_streamk(cudaStream_t st, const MttkrpArgs& a, int varia
 //   256     3.5  | 33.59              | 34.41              | 33.84
 //   128     1.7  | 32.23              | 29.56              | 32.05
 //   4096   55    | 35.53              | 35.81              | --
+// Deeper rings at 256 rows do not help (BK 8: 6 stages 34.93, 5 stages 35.02;
+// the stream-K form with BK 8 / 6 stages 34.67), so the per-k-tile overhead,
+// not the bytes in flight, is what the wider l-tiles save.
 // Round-1 baseline (the per-i kernel, fused kernel configs 0-7 and the LDGSTS
 // bodies): 34.8 / 30.9 / 33.4.
 static int default_mttkrp_config(const MttkrpArgs& a) {
