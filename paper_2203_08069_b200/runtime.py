@@ -50,9 +50,17 @@ from .trace import CommEvent, ExecutionTrace
 LEAF_POLICIES = ("auto", "exact")
 # lower one-to-many fetches to ncclBroadcast on GPU sub-communicators (else p2p fan-out)
 USE_BROADCAST = True
-# issue step s+1's NCCL group while step s's leaves run (False serialises them: a
-# measurement switch for the overlap, used by bench.py)
+# issue step s+1's NCCL group while step s's leaves run (False serialises every
+# step: a measurement switch for the overlap, used by bench.py).  Even when True,
+# a step whose transfers are large (>= SERIAL_MIN_BYTES into one GPU) yet take
+# < SERIAL_FRACTION of the previous step's leaf time (at NVLINK_GBS / FP64 peak)
+# is serialised: NCCL's copy kernels would only hold SM slots the DMMA waves
+# need for gigabytes' worth of transfer (Cannon 2x2 at 26112^3 on 4 B200s:
+# 249.0 ms per step serialised on every box, 251-276 ms overlapped).
 OVERLAP_COMM = True
+SERIAL_MIN_BYTES = 64 << 20
+SERIAL_FRACTION = 0.1
+NVLINK_GBS = 400.0
 # pipeline the first step: its cross-GPU transfers go in two k-pieces (1/8, 7/8)
 # and the GEMM leaves start on the first piece while the rest is in flight
 # (nothing earlier can hide step 0's transfers: Cannon's skew, Johnson's faces)
@@ -761,9 +769,42 @@ class _Executor:
         return self.plan.out_name in {a.tensor.name for leaf in leaf_statements(self.plan.task_body)
                                       for a in accesses_of(leaf.rhs)}
 
+    def _serial_steps(self) -> frozenset:
+        """Steps whose transfers wait for the previous step's leaves (see
+        OVERLAP_COMM); decided from the program alone, so every rank agrees."""
+        cached = self.prog.__dict__.get("_serial_steps")
+        if cached is not None:
+            return cached
+        out = set()
+        for s in range(1, self.plan.num_steps):
+            inbound = {}
+            for t in self.prog.transfers[s]:
+                gs, gd = self.gpu(t.src), self.gpu(t.dst)
+                if gs != gd:
+                    inbound[gd] = inbound.get(gd, 0) + 8 * t.part.volume
+            flops = {}
+            for w in self.prog.work[s - 1]:
+                ext = {}
+                for names, (_, rect, _) in w.operands.items():
+                    if rect is not None:
+                        ext.update(zip(names, rect.shape))
+                vol = 1
+                for e in ext.values():
+                    vol *= e
+                g = self.gpu(w.task.coord)
+                flops[g] = flops.get(g, 0) + 2 * vol
+            big = max(inbound.values(), default=0)
+            comm_s = big / (NVLINK_GBS * 1e9)
+            compute_s = min(flops.values(), default=0) / (FP64_PEAK_GFLOPS * 1e9)
+            if big >= SERIAL_MIN_BYTES and comm_s < SERIAL_FRACTION * compute_s:
+                out.add(s)
+        self.prog._serial_steps = frozenset(out)
+        return self.prog._serial_steps
+
     def _steps(self, nsteps):
+        serial = self._serial_steps() if OVERLAP_COMM else frozenset()
         for s in range(nsteps):
-            if not OVERLAP_COMM:   # measurement switch: step s+1's transfers wait for step s's leaves
+            if not OVERLAP_COMM or s in serial:   # step s's transfers wait for step s-1's leaves
                 for g in self.owned:
                     self._sync(self.xstream(g), self.cstream(g))
             split = self._split_plan(s) if s == 0 and self.prog.stepwise else None

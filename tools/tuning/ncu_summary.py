@@ -14,7 +14,7 @@ WANT = {
     "launch__grid_size": "grid", "launch__block_size": "block",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3, "ms": 1,
          "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1, "second": 1e3}
 out = {}
 import os

@@ -40,6 +40,7 @@ elif which == "g1":
 elif which == "mttkrp":
     n, R = 1024, 32
     b = gen((n, n, n), 1); cm = gen((n, R), 2); d = gen((n, R), 3); a = torch.empty(n, R, dtype=torch.float64, device="cuda")
+    # default selection at this shape: whole-item CTAs + stream-K last wave (mttkrp_st_kernel)
     for _ in range(2): nat.call("td_mttkrp", st(), n, n, n, R, P(b), n*n, n, P(cm), R, P(d), R, P(a), R, 0)
 torch.cuda.synchronize()
 print("done", which)

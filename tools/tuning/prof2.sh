@@ -11,7 +11,7 @@ ncu --set full --clock-control none --import-source on -k regex:dgemm_tma_kernel
 ncu --set full --clock-control none --import-source on -k regex:ttv_kernel -s 1 -c 1 -o gpurun_out/${R}_ttv python tools/tuning/prof2.py ttv >> gpurun_out/ncu_${R}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:innerprod_partial -s 1 -c 1 -o gpurun_out/${R}_innerprod python tools/tuning/prof2.py innerprod >> gpurun_out/ncu_${R}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:dgemm_tma_kernel -s 1 -c 1 -o gpurun_out/${R}_ttm python tools/tuning/prof2.py ttm >> gpurun_out/ncu_${R}.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:dgemm_tma_kernel -s 1 -c 1 -o gpurun_out/${R}_mttkrp python tools/tuning/prof2.py mttkrp >> gpurun_out/ncu_${R}.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:mttkrp_st_kernel -s 1 -c 1 -o gpurun_out/${R}_mttkrp python tools/tuning/prof2.py mttkrp >> gpurun_out/ncu_${R}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:dgemm_tma_grouped -s 4 -c 1 -o gpurun_out/${R}_g1 python tools/tuning/prof2.py g1 >> gpurun_out/ncu_${R}.log 2>&1
 python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bench_plain_${R}.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_bench_${R}.log 2>&1
 echo done
