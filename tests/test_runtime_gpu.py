@@ -279,3 +279,27 @@ def test_nvtx_ranges_do_not_change_results():
     finally:
         runtime.NVTX = False
     assert np.array_equal(res.output.data, ins["A"].data @ ins["B"].data)
+
+
+def test_lazy_zero_reads_and_launches():
+    """RegionStore.zero only marks the pieces (the next launch's first leaf
+    overwrites them): reads before any launch (gather, local_pieces) still
+    see +0.0, and zero -> execute equals a fresh run, eagerly and from
+    replayed launch plans, on every bundle shape."""
+    for b in (td.summa(2, 2, dims=(24, 20, 28), chunk=8), td.johnson(2, 2, 2, dims=(16, 12, 20)),
+              td.mttkrp(2, 2, dims=(12, 8, 10, 9)), td.ttv(2, dims=(6, 5, 7)),
+              td.innerprod3(2, dims=(8, 6, 30))):
+        cin, store = b.prepare(seed=9)
+        out = b.statement.lhs.tensor.name
+        td.execute(cin, store, record_requirements=False)
+        want = store.gather(out).data.copy()
+        store.zero(out)
+        assert not store.gather(out).data.any(), b.name          # materialised on read
+        store.zero(out)
+        for _ in range(3):                                          # eager, then plan replays
+            store.zero(out)
+            td.execute(cin, store, record_requirements=False)
+            assert np.array_equal(store.gather(out).data, want), b.name
+        store.zero(out)
+        for _, piece in store.local_pieces(out):
+            assert not piece.any(), b.name
