@@ -414,7 +414,10 @@ static int launch_mttkrp_streamk(cudaStream_t st, const MttkrpArgs& a, int varia
 //   4096   55    | 35.53              | 35.81              | --
 // Deeper rings at 256 rows do not help (BK 8: 6 stages 34.93, 5 stages 35.02;
 // the stream-K form with BK 8 / 6 stages 34.67), so the per-k-tile overhead,
-// not the bytes in flight, is what the wider l-tiles save.
+// not the bytes in flight, is what the wider l-tiles save.  A dedicated producer
+// warp (warp-specialised 128-row tiles, 4 compute warps + 1 TMA warp, 3 CTAs/SM,
+// all slots in flight) is slower too: 34.53 (BK 16) / 33.75 (BK 8, 6 stages) vs
+// 34.99 with the issuing thread inside warp 0; 35.07 vs 35.53 at I = 4096.
 // Round-1 baseline (the per-i kernel, fused kernel configs 0-7 and the LDGSTS
 // bodies): 34.8 / 30.9 / 33.4.
 static int default_mttkrp_config(const MttkrpArgs& a) {
