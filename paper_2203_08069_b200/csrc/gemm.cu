@@ -300,6 +300,9 @@ static int raster_group(int blocks_per_sm, int BM, int BN) {
   // Measured on B200 at 16384^3 with 64x64 tiles (tools/tuning/group_sweep.sh):
   // DRAM read per launch 558/290/164/115/128/263 GB for groups 1/2/4/8/16/32
   // with the same 35.5 TFLOP/s -- 8 M-tiles per group minimises re-reads.
+  // Round 2, TMA kernel (4 CTAs/SM): 164/119/130/160/218/288 GB for groups
+  // 4/8/12/16/24/32 at an unchanged 36.40 TFLOP/s (the squarer waves re-read
+  // more: concurrently running CTAs drift apart in k) -- 8 again.
   (void)blocks_per_sm;
   (void)BM;
   (void)BN;
