@@ -96,6 +96,14 @@ typedef struct td_gemm_problem {
   int64_t ldb;
   double* C;
   int64_t ldc;
+  /* optional second k-segment (K2 = 0: none), accumulated in the same registers
+   * after the first: C (+)= A.B + A2.B2, A2 M x K2, B2 K2 x N (two k-slabs of a
+   * task's steps that live in different pieces -> one launch instead of two) */
+  int64_t K2;
+  const double* A2;
+  int64_t lda2;
+  const double* B2;
+  int64_t ldb2;
 } td_gemm_problem;
 int td_dgemm_grouped(void* stream, int count, const td_gemm_problem* problems, int accumulate);
 

@@ -137,7 +137,8 @@ class TdOp(C.Structure):
 
 class TdGemmProblem(C.Structure):
     _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("A", C.c_void_p), ("lda", C.c_int64),
-                ("B", C.c_void_p), ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64)]
+                ("B", C.c_void_p), ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
+                ("K2", C.c_int64), ("A2", C.c_void_p), ("lda2", C.c_int64), ("B2", C.c_void_p), ("ldb2", C.c_int64)]
 
 
 _SIGNATURES["td_dgemm_grouped"] = ([vp, i32, C.POINTER(TdGemmProblem), i32], i32)

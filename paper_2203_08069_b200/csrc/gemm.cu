@@ -618,17 +618,29 @@ int td_dgemm_grouped(void* stream, int count, const td_gemm_problem* problems, i
   TD_REQUIRE(count >= 0 && count <= TD_GEMM_GROUP_MAX && (count == 0 || problems),
              "dgemm_grouped: 0..%d problems", TD_GEMM_GROUP_MAX);
   td::StreamDevice sd(stream);
+  const cudaStream_t st = td::as_stream(stream);
   td::GemmArgs args[TD_GEMM_GROUP_MAX];
   int n = 0;
-  bool tma = true;
+  bool tma = true, seg2 = false;
   int64_t maxN = 0;
   for (int q = 0; q < count; ++q) {
     const td_gemm_problem& pr = problems[q];
     td::GemmArgs a{pr.M, pr.N, pr.K, pr.A, pr.lda, 0, pr.B, pr.ldb, 0, pr.C, pr.ldc, 0, accumulate, 0, 0, 0,
                    nullptr, 0};
     if (a.M <= 0 || a.N <= 0) continue;
+    if (pr.K2 > 0) {
+      if (a.K <= 0) {  // only the second segment
+        a.K = pr.K2; a.A = pr.A2; a.lda = pr.lda2; a.B = pr.B2; a.ldb = pr.ldb2;
+      } else {
+        a.K2 = pr.K2; a.A2 = pr.A2; a.lda2 = pr.lda2; a.B2 = pr.B2; a.ldb2 = pr.ldb2;
+        td::GemmArgs s2 = a;
+        s2.K = a.K2; s2.A = a.A2; s2.lda = a.lda2; s2.B = a.B2; s2.ldb = a.ldb2;
+        tma = tma && td::tma_ok(1, s2);
+        seg2 = true;
+      }
+    }
     if (a.K <= 0) {  // nothing to multiply: only the Assign form writes zeros
-      if (int rc = td::dgemm_dispatch(td::as_stream(stream), 1, a)) return rc;
+      if (int rc = td::dgemm_dispatch(st, 1, a)) return rc;
       continue;
     }
     tma = tma && td::tma_ok(1, a);
@@ -636,14 +648,27 @@ int td_dgemm_grouped(void* stream, int count, const td_gemm_problem* problems, i
     args[n++] = a;
   }
   if (n == 0) return TD_OK;
-  if (!tma || n == 1) {  // one problem, or one TMA cannot address: separate launches
-    for (int q = 0; q < n; ++q)
-      if (int rc = td::dgemm_dispatch(td::as_stream(stream), 1, args[q])) return rc;
+  if (!tma || (n == 1 && !seg2)) {  // one plain problem, or one TMA cannot address: separate launches
+    for (int q = 0; q < n; ++q) {
+      td::GemmArgs a = args[q];
+      const int64_t K2 = a.K2;
+      a.K2 = 0;
+      if (int rc = td::dgemm_dispatch(st, 1, a)) return rc;
+      if (K2 > 0) {  // the second segment accumulates after the first (same stream)
+        a.K = K2; a.A = args[q].A2; a.lda = args[q].lda2; a.B = args[q].B2; a.ldb = args[q].ldb2;
+        a.accumulate = 1;
+        if (int rc = td::dgemm_dispatch(st, 1, a)) return rc;
+      }
+    }
     return TD_OK;
   }
   // the default TMA tiles (config 47 / 48 by N, gemm.cu default_tma_config)
-  if (maxN <= 32) return td::launch_gemm_tma_grouped<128, 32, 16, 32, 32, 3, 4>(td::as_stream(stream), n, args);
-  return td::launch_gemm_tma_grouped<64, 64, 16, 32, 32, 3, 4>(td::as_stream(stream), n, args);
+  if (seg2) {
+    if (maxN <= 32) return td::launch_gemm_tma_grouped<128, 32, 16, 32, 32, 3, 4, true>(st, n, args);
+    return td::launch_gemm_tma_grouped<64, 64, 16, 32, 32, 3, 4, true>(st, n, args);
+  }
+  if (maxN <= 32) return td::launch_gemm_tma_grouped<128, 32, 16, 32, 32, 3, 4>(st, n, args);
+  return td::launch_gemm_tma_grouped<64, 64, 16, 32, 32, 3, 4>(st, n, args);
 }
 
 int td_ttm(void* stream, int64_t I, int64_t J, int64_t K, int64_t L, const double* B, int64_t sBi,

@@ -28,6 +28,13 @@ struct GemmArgs {
   double* out;
   int64_t ldo;
   int out_acc;
+  // TMA body, grouped kernel: an optional second k-segment (K2 > 0) accumulated
+  // after the first in the same registers (td_gemm_problem.K2)
+  int64_t K2;
+  const double* A2;
+  int64_t lda2;
+  const double* B2;
+  int64_t ldb2;
 };
 
 // MTTKRP row-sum GEMMs (EPI = 1 in gemm.cu): rows per M-tile of a config, launch

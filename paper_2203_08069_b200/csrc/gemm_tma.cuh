@@ -175,9 +175,10 @@ __device__ __forceinline__ void tma_epilogue(double (&acc)[TmaCfg<BM, BN, BK, WM
 // entry `bz`, operands through the tensor maps tmA / tmB (kernel-parameter
 // addresses: __grid_constant__).  Shared by the plain kernel and the
 // grouped one below.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int EPI, int MINB, bool SEG2 = false>
 __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUtensorMap* tmB_, const GemmArgs& p,
-                                              const int tile, const int bz) {
+                                              const int tile, const int bz, const CUtensorMap* tmA2 = nullptr,
+                                              const CUtensorMap* tmB2 = nullptr) {
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   extern __shared__ __align__(128) unsigned char tma_smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES];
@@ -206,7 +207,8 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
   const int warp = tid >> 5;
   const int wm0 = (warp / Cfg::WARPS_N) * WM;
   const int wn0 = (warp % Cfg::WARPS_N) * WN;
-  const int ktiles = (int)ceil_div(K, BK);
+  const int kt1 = (int)ceil_div(K, BK);  // k-tiles of the first segment
+  const int ktiles = kt1 + (SEG2 && p.K2 > 0 ? (int)ceil_div(p.K2, BK) : 0);
 
   if (tid == 0) {
 #pragma unroll
@@ -221,6 +223,11 @@ __device__ __forceinline__ void tma_gemm_tile(const CUtensorMap* tmA_, const CUt
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
     mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    if (SEG2 && kt >= kt1) {  // second segment: its own operands, k from 0 again
+      tma_load_4d(As + s * Cfg::A_STAGE, tmA2, 0, m0, (kt - kt1) * (BK / 4), bz, &full[s]);
+      tma_load_4d(Bs + s * Cfg::B_STAGE, tmB2, 0, (kt - kt1) * BK, n0 / 4, bzB, &full[s]);
+      return;
+    }
     tma_load_4d(As + s * Cfg::A_STAGE, &tmA, 0, m0, kt * (BK / 4), bz, &full[s]);
     tma_load_4d(Bs + s * Cfg::B_STAGE, &tmB, 0, kt * BK, n0 / 4, bzB, &full[s]);
   };
@@ -280,22 +287,25 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
 // Grouped launch: up to TD_GEMM_GROUP_MAX problems, their tiles laid end to
 // end along grid.x (problem q owns tiles [start[q], start[q+1])).
-struct alignas(64) GroupedTma {
+template <bool SEG2>
+struct alignas(64) GroupedTmaT {
   CUtensorMap map[2 * TD_GEMM_GROUP_MAX];
+  CUtensorMap map2[SEG2 ? 2 * TD_GEMM_GROUP_MAX : 1];  // second k-segments (SEG2 only)
   GemmArgs args[TD_GEMM_GROUP_MAX];
   int start[TD_GEMM_GROUP_MAX + 1];
   int count;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0, bool SEG2 = false>
 __global__ void __launch_bounds__(TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::THREADS,
                                   TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>::MIN_BLOCKS)
-dgemm_tma_grouped_kernel(const __grid_constant__ GroupedTma g) {
+dgemm_tma_grouped_kernel(const __grid_constant__ GroupedTmaT<SEG2> g) {
   const int x = blockIdx.x;
   int q = 0;
   while (q + 1 < g.count && x >= g.start[q + 1]) ++q;
   const GemmArgs p = g.args[q];
-  tma_gemm_tile<BM, BN, BK, WM, WN, STAGES, 0, MINB>(&g.map[2 * q], &g.map[2 * q + 1], p, x - g.start[q], 0);
+  tma_gemm_tile<BM, BN, BK, WM, WN, STAGES, 0, MINB, SEG2>(&g.map[2 * q], &g.map[2 * q + 1], p, x - g.start[q], 0,
+                                                           &g.map2[SEG2 ? 2 * q : 0], &g.map2[SEG2 ? 2 * q + 1 : 0]);
 }
 
 // ---- host side: tensor maps through the driver entry point (no -lcuda)
@@ -401,12 +411,12 @@ static int launch_gemm_tma(cudaStream_t st, int64_t batch, GemmArgs a) {
 namespace td {
 
 // Grouped form of launch_gemm_tma (plain epilogue, batch 1 per problem).
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB = 0, bool SEG2 = false>
 static int launch_gemm_tma_grouped(cudaStream_t st, int count, const GemmArgs* probs) {
   using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, MINB>;
-  auto kern = dgemm_tma_grouped_kernel<BM, BN, BK, WM, WN, STAGES, MINB>;
+  auto kern = dgemm_tma_grouped_kernel<BM, BN, BK, WM, WN, STAGES, MINB, SEG2>;
   TD_CUDA(ensure_smem(kern, Cfg::SMEM_BYTES));
-  GroupedTma g;
+  GroupedTmaT<SEG2> g;
   std::memset(&g, 0, sizeof g);
   g.count = count;
   int64_t tiles = 0;
@@ -414,6 +424,14 @@ static int launch_gemm_tma_grouped(cudaStream_t st, int count, const GemmArgs* p
     GemmArgs a = probs[q];
     if (int rc = make_sliced_map(&g.map[2 * q], a.A, a.M, a.K, a.lda, 1, 0, BM, BK)) return rc;
     if (int rc = make_sliced_map(&g.map[2 * q + 1], a.B, a.K, a.N, a.ldb, 1, 0, BK, BN)) return rc;
+    if constexpr (SEG2) {
+      if (a.K2 > 0) {
+        if (int rc = make_sliced_map(&g.map2[2 * q], a.A2, a.M, a.K2, a.lda2, 1, 0, BM, BK)) return rc;
+        if (int rc = make_sliced_map(&g.map2[2 * q + 1], a.B2, a.K2, a.N, a.ldb2, 1, 0, BK, BN)) return rc;
+      }
+    } else {
+      a.K2 = 0;
+    }
     a.tiles_m = (int)ceil_div(a.M, BM);
     a.tiles_n = (int)ceil_div(a.N, BN);
     a.group = raster_group(Cfg::MIN_BLOCKS, BM, BN);

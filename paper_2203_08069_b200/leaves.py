@@ -48,7 +48,10 @@ _ENUM_LIMIT = 1 << 22
 
 # counters for the bench / tests: which path each step took
 STATS = {"dgemm": 0, "ttv": 0, "ttm": 0, "mttkrp": 0, "innerprod": 0, "contract": 0, "nest": 0, "grouped": 0,
-         "k_merged": 0}
+         "k_merged": 0, "folded": 0}
+# a tile's two remaining k-segments (after k-merging) go out as one two-segment
+# grouped problem (td_gemm_problem.K2) instead of two rounds (a measurement switch)
+FOLD_SEGMENTS = True
 
 
 # optional per-launch device timing: set TIMING = [] to collect
@@ -485,6 +488,11 @@ def _k_adjacent(first, nxt) -> bool:
             and nxt[6] == ldb and nxt[3] == a + 8 * k and nxt[5] == b + 8 * k * ldb)
 
 
+def _same_tile(first, nxt) -> bool:
+    """Do two GEMMs write the same output tile (M, N, C, ldc)?"""
+    return first[0] == nxt[0] and first[1] == nxt[1] and first[7] == nxt[7] and first[8] == nxt[8]
+
+
 def _flush_gemms(pending) -> None:
     """Issue deferred GEMMs: per output tile, consecutive GEMMs continuing
     each other along k (a task's steps reading k-slabs of the same resident
@@ -504,6 +512,12 @@ def _flush_gemms(pending) -> None:
                     STATS["k_merged"] += 1
                 else:
                     merged.append([acc, prob])
+            if FOLD_SEGMENTS and len(merged) == 2 and merged[1][0] == 1 and _same_tile(merged[0][1], merged[1][1]):
+                # two k-segments of one tile from different pieces: one problem, the
+                # second accumulated after the first in the same registers
+                _, _, k2, a2, lda2, b2, ldb2, _, _ = merged[1][1]
+                merged = [[merged[0][0], merged[0][1] + (k2, a2, lda2, b2, ldb2)]]
+                STATS["folded"] += 1
             seq[:] = merged
         depth = max(len(seq) for seq in per_c.values())
         for r in range(depth):
@@ -528,7 +542,7 @@ def flush_pending() -> None:
 
 
 def _launch_group(stream, chunk, acc) -> None:
-    if len(chunk) == 1:
+    if len(chunk) == 1 and len(chunk[0]) == 9:
         m, n, k, a, lda, b, ldb, c, ldc = chunk[0]
         _native.call("td_dgemm", stream_handle(stream), m, n, k, C.c_void_p(a), lda, C.c_void_p(b), ldb,
                      C.c_void_p(c), ldc, acc)

@@ -131,6 +131,42 @@ def test_grouped_gemm_equals_separate_launches():
         assert torch.equal(c0, c1)
 
 
+@pytest.mark.parametrize("shapes", [
+    [(512, 512, 512, 512)],                                        # one problem: still one folded launch
+    [(512, 512, 512, 512), (512, 512, 128, 0), (256, 384, 96, 200), (200, 120, 64, 36)],
+    [(300, 32, 64, 48), (128, 24, 40, 16)],                        # N <= 32 tiles
+    [(128, 128, 64, 33)],                                          # K2 odd: TMA cannot take it -> two launches
+])
+def test_grouped_gemm_two_segments_exact(shapes):
+    """td_dgemm_grouped with td_gemm_problem.K2: C (+)= A.B + A2.B2 with the
+    two k-segments from unrelated buffers (a tile's two steps in different
+    pieces, folded into one problem), exact on integer data, mixed with
+    single-segment problems, ragged K / K2, and the fallback for operands the
+    copy engine cannot address."""
+    lib = _native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    probs = (_native.TdGemmProblem * len(shapes))()
+    keep, want = [], []
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ints = lambda *s: torch.randint(-4, 5, s, generator=g, device="cuda").to(torch.float64)  # noqa: E731
+    for q, (m, n, k, k2) in enumerate(shapes):
+        a, b, c = ints(m, k), ints(k, n), ints(m, n)
+        a2, b2 = ints(m, max(k2, 1)), ints(max(k2, 1), n)
+        keep += [a, b, c, a2, b2]
+        want.append(c.cpu().numpy() + a.cpu().numpy() @ b.cpu().numpy()
+                    + (a2.cpu().numpy() @ b2.cpu().numpy() if k2 else 0))
+        probs[q].M, probs[q].N, probs[q].K = m, n, k
+        probs[q].A, probs[q].lda, probs[q].B, probs[q].ldb = a.data_ptr(), k, b.data_ptr(), n
+        probs[q].C, probs[q].ldc = c.data_ptr(), n
+        if k2:
+            probs[q].K2, probs[q].A2, probs[q].lda2 = k2, a2.data_ptr(), a2.shape[1]
+            probs[q].B2, probs[q].ldb2 = b2.data_ptr(), n
+    assert lib.td_dgemm_grouped(C.c_void_p(st), len(shapes), probs, 1) == 0, lib.td_last_error()
+    torch.cuda.synchronize()
+    for q, w in enumerate(want):
+        assert np.array_equal(keep[5 * q + 2].cpu().numpy(), w), shapes[q]
+
+
 def test_plan_cache_follows_the_store_and_switches():
     """A plan is keyed on the program, the output's freshness, the pieces'
     addresses and the streams: re-placing an input (new buffers) records a
