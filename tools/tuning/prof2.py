@@ -30,11 +30,11 @@ elif which == "ttm":
     for _ in range(2): nat.call("td_ttm", st(), n, n, n, L, P(b), n*n, n, P(cm), L, P(y), n*L, L, 0)
 elif which == "g1":
     # BASELINE G1 (SUMMA 1024^3 on 2x2, chunk 128) through the runtime: launch plans
-    # replay its 2 grouped k-merged DMMA launches (dgemm_tma_grouped_kernel)
+    # replay its one grouped, k-merged, two-segment DMMA launch (dgemm_tma_grouped_kernel)
     import paper_2203_08069_b200 as td
     b = td.summa(2, 2, dims=(1024,) * 3, chunk=128)
     cin, store = b.prepare(seed=0, mode=0)
-    for _ in range(4):
+    for _ in range(8):
         store.zero("C")
         td.execute(cin, store, record_requirements=False)
 elif which == "mttkrp":
