@@ -28,6 +28,7 @@ whole output box, and the task runs exactly one leaf (so the leaf can
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from collections import Counter
 
@@ -36,6 +37,12 @@ from . import _native
 # leaves whose whole partial is reduced into another GPU's piece write it there
 # directly (False: leaf into a local buffer, then an NCCL send; a measurement switch)
 PEER_REDUCE = True
+# big single-destination transfers after step 0 (Cannon's shifts) go GPU to GPU by
+# copy engine into a persistent buffer on the receiver, ordered by 8-byte NCCL
+# tokens: no SM slot is held while the DMMA waves run (SPMD jobs; False: NCCL
+# send/recv, then serialised behind the leaves, runtime._serial_steps)
+CE_SHIFTS = os.environ.get("TD_CE_SHIFTS", "1") != "0"
+SHIFT_MIN_BYTES = 64 << 20
 
 IPC_HANDLE_BYTES = 64
 
@@ -117,11 +124,40 @@ def eligible_commits(prog, gpu_of) -> dict:
     return out
 
 
-class Inbox:
-    """One write-back buffer in the home GPU's HBM, mapped on the writer GPU."""
+def eligible_shifts(prog, gpu_of) -> dict:
+    """{(step, index): Transfer} of the transfers that go by copy engine: after
+    step 0 (step 0's are pipelined with its leaves), cross-GPU, not relayed,
+    one destination GPU for their source box, >= SHIFT_MIN_BYTES."""
+    out = {}
+    for s, moves in enumerate(prog.transfers):
+        if s == 0:
+            continue
+        dsts = {}
+        for t in moves:
+            gs, gd = gpu_of(t.src), gpu_of(t.dst)
+            if gs != gd:
+                dsts.setdefault((gs, t.src_hid, t.part), set()).add(gd)
+        for i, t in enumerate(moves):
+            gs, gd = gpu_of(t.src), gpu_of(t.dst)
+            if gs == gd or t.wave != 0 or len(dsts[(gs, t.src_hid, t.part)]) != 1:
+                continue
+            if 8 * t.part.volume >= SHIFT_MIN_BYTES:
+                out[(s, i)] = t
+    return out
 
-    def __init__(self, commit, home_gpu, writer_gpu, shape):
+
+def _shifts_apply(world) -> bool:
+    """Copy-engine shifts run in SPMD jobs (one GPU per process)."""
+    return CE_SHIFTS and world.nprocs > 1 and world.nprocs == world.ngpus
+
+
+class Inbox:
+    """One write-back buffer in the home GPU's HBM, mapped on the writer GPU
+    (a commit's partial, or -- `transfer` set -- a copy-engine shift's box)."""
+
+    def __init__(self, commit, home_gpu, writer_gpu, shape, transfer=None):
         self.commit = commit
+        self.transfer = transfer
         self.home_gpu = home_gpu
         self.writer_gpu = writer_gpu
         self.shape = tuple(shape)
@@ -171,7 +207,8 @@ class InboxSet:
         self.inboxes = {}
         self.pins = 0          # captured graphs / recorded plans holding raw inbox pointers
         cand = eligible_commits(prog, gpu_of)
-        if not cand:
+        shifts = eligible_shifts(prog, gpu_of) if _shifts_apply(world) else {}
+        if not cand and not shifts:
             return
         W = world
         multi = W.nprocs > 1
@@ -179,13 +216,14 @@ class InboxSet:
         handles = {}
         ok = True
         for k, c in sorted(cand.items()):
-            gh, gt = gpu_of(c.home), gpu_of(c.task.coord)
-            ib = Inbox(c, gh, gt, c.part.shape)
-            if W.owns(gh):
-                ib.home_dev = W.device(gh)
-            if W.owns(gt):
-                ib.writer_dev = W.device(gt)
-            boxes[k] = ib
+            boxes[("c", k)] = Inbox(c, gpu_of(c.home), gpu_of(c.task.coord), c.part.shape)
+        for (s, i), t in sorted(shifts.items()):
+            boxes[("x", s, i)] = Inbox(None, gpu_of(t.dst), gpu_of(t.src), t.part.shape, transfer=t)
+        for ib in boxes.values():
+            if W.owns(ib.home_gpu):
+                ib.home_dev = W.device(ib.home_gpu)
+            if W.owns(ib.writer_gpu):
+                ib.writer_dev = W.device(ib.writer_gpu)
         # single process: both ends owned -> plain peer access
         for k, ib in boxes.items():
             if ib.home_dev is not None and ib.writer_dev is not None:
@@ -245,7 +283,10 @@ class InboxSet:
         self.inboxes = boxes
 
     def by_task(self) -> dict:
-        return {ib.commit.task.coord: ib for ib in self.inboxes.values()}
+        return {ib.commit.task.coord: ib for ib in self.inboxes.values() if ib.commit is not None}
+
+    def by_transfer(self) -> dict:
+        return {id(ib.transfer): ib for ib in self.inboxes.values() if ib.transfer is not None}
 
     def pin(self):
         self.pins += 1
@@ -295,6 +336,9 @@ class _Empty:
     def by_task(self) -> dict:
         return {}
 
+    def by_transfer(self) -> dict:
+        return {}
+
 
 _NO_INBOXES = _Empty()
 
@@ -308,8 +352,8 @@ def inbox_set(prog, world, gpu_of) -> InboxSet:
     hit = reg.get(id(prog))
     if hit is not None and hit.prog is prog:
         return hit
-    if not eligible_commits(prog, gpu_of):     # nothing to map: do not evict a useful set
-        return _NO_INBOXES
+    if not eligible_commits(prog, gpu_of) and not (_shifts_apply(world) and eligible_shifts(prog, gpu_of)):
+        return _NO_INBOXES                     # nothing to map: do not evict a useful set
     while len(reg) >= MAX_SETS:
         # the least recently created set no rank pins (a CUDA graph or launch plan
         # holding its raw pointers keeps it alive; then the registry grows); the

@@ -52,11 +52,12 @@ LEAF_POLICIES = ("auto", "exact")
 USE_BROADCAST = True
 # issue step s+1's NCCL group while step s's leaves run (False serialises every
 # step: a measurement switch for the overlap, used by bench.py).  Even when True,
-# a step whose transfers are large (>= SERIAL_MIN_BYTES into one GPU) yet take
-# < SERIAL_FRACTION of the previous step's leaf time (at NVLINK_GBS / FP64 peak)
-# is serialised: NCCL's copy kernels would only hold SM slots the DMMA waves
-# need for gigabytes' worth of transfer (Cannon 2x2 at 26112^3 on 4 B200s:
-# 249.0 ms per step serialised on every box, 251-276 ms overlapped).
+# a step whose NCCL transfers are large (>= SERIAL_MIN_BYTES into one GPU) yet
+# take < SERIAL_FRACTION of the previous step's leaf time (at NVLINK_GBS / FP64
+# peak) is serialised: NCCL's copy kernels would only hold SM slots the DMMA
+# waves need for gigabytes' worth of transfer (Cannon 2x2 at 26112^3 on 4 B200s:
+# 249.0 ms per step serialised on every box, 251-276 ms overlapped).  Copy-engine
+# shifts (peer.CE_SHIFTS) hold no SM slot and stay overlapped.
 OVERLAP_COMM = True
 SERIAL_MIN_BYTES = 64 << 20
 SERIAL_FRACTION = 0.1
@@ -581,6 +582,8 @@ def g_index(world, g) -> int:
 
 
 class _Executor:
+    shift: dict = {}            # id(Transfer) -> copy-engine shift buffer (set per launch by run)
+
     def __init__(self, prog, store: RegionStore, policy: str):
         self.prog = prog
         self.plan = prog.plan
@@ -671,6 +674,7 @@ class _Executor:
         self.store.row_done = {k: v for k, v in self.store.row_done.items() if k[0] != self.plan.out_name}
         self.direct = self._direct_commits(out_region)
         self.inbox = self._inboxes()
+        self.shift = self._shifts()
         self.overwrite = self._lazy_zeros(out_region)
         for t in self.plan.tasks:
             g = self.gpu(t.coord)
@@ -705,6 +709,7 @@ class _Executor:
             if not self.prog.stepwise:
                 self.compute(self.prog.work[-1], -1)
             self._fill_unwritten()
+            self._shift_credits()
             with _nvtx("commit"):
                 self.commit(out_region)
             self._mark_done(out_region, self.prog.commits)
@@ -772,18 +777,22 @@ class _Executor:
     def _serial_steps(self) -> frozenset:
         """Steps whose transfers wait for the previous step's leaves (see
         OVERLAP_COMM); decided from the program alone, so every rank agrees."""
+        ce = bool(self.shift)
         cached = self.prog.__dict__.get("_serial_steps")
-        if cached is not None:
-            return cached
+        if cached is not None and cached[0] == ce:
+            return cached[1]
         out = set()
-        for s in range(1, self.plan.num_steps):
+        for s in range(self.plan.num_steps):
+            # step 0 overlaps the previous launch's leaves (back-to-back launches): the
+            # same contention, measured against its own leaves (Johnson 2x2x2 on 4 GPUs:
+            # 492 ms per step serialised, 506-579 ms overlapped on the same box)
             inbound = {}
             for t in self.prog.transfers[s]:
                 gs, gd = self.gpu(t.src), self.gpu(t.dst)
-                if gs != gd:
+                if gs != gd and id(t) not in self.shift:   # copy-engine shifts hold no SM slots
                     inbound[gd] = inbound.get(gd, 0) + 8 * t.part.volume
             flops = {}
-            for w in self.prog.work[s - 1]:
+            for w in self.prog.work[max(s - 1, 0)]:
                 ext = {}
                 for names, (_, rect, _) in w.operands.items():
                     if rect is not None:
@@ -798,8 +807,8 @@ class _Executor:
             compute_s = min(flops.values(), default=0) / (FP64_PEAK_GFLOPS * 1e9)
             if big >= SERIAL_MIN_BYTES and comm_s < SERIAL_FRACTION * compute_s:
                 out.add(s)
-        self.prog._serial_steps = frozenset(out)
-        return self.prog._serial_steps
+        self.prog._serial_steps = (ce, frozenset(out))
+        return self.prog._serial_steps[1]
 
     def _steps(self, nsteps):
         serial = self._serial_steps() if OVERLAP_COMM else frozenset()
@@ -833,6 +842,34 @@ class _Executor:
         if plugins:             # user leaf kernels are handed PyTorch tensors
             return {}
         return peer.inbox_set(self.prog, self.W, self.gpu).by_task()
+
+    def _shifts(self) -> dict:
+        """{id(Transfer): peer.Inbox} of the transfers that go by copy engine
+        into a persistent buffer on the receiving GPU (`peer.CE_SHIFTS`)."""
+        if not (self.W.multi_gpu and self.prog.stepwise) or not peer._shifts_apply(self.W):
+            return {}
+        task_loops, _ = _loops_of(self.plan.task_body)
+        _, plugins = _leaf_choice(self.plan.relations, [v for v, _, _ in task_loops], self.policy)
+        if plugins:             # user leaf kernels are handed PyTorch tensors
+            return {}
+        return peer.inbox_set(self.prog, self.W, self.gpu).by_transfer()
+
+    def _shift_credits(self) -> None:
+        """End of launch: every receiver has read its shift buffers (its
+        compute stream is done) -- an 8-byte NCCL credit per shift lets the
+        sender's next copy (stream-ordered after it on the sender's
+        communication stream) overwrite the buffer."""
+        if not self.shift:
+            return
+        for g in self.owned:
+            self._sync(self.xstream(g), self.cstream(g))
+        sends, recvs = [], []
+        for ib in self.shift.values():
+            if self.W.owns(ib.home_gpu):
+                sends.append((ib.home_gpu, ib.writer_gpu, self._token(ib.home_gpu)))
+            if self.W.owns(ib.writer_gpu):
+                recvs.append((ib.writer_gpu, ib.home_gpu, self._token(ib.writer_gpu)))
+        self._nccl(sends, recvs)
 
     def _local_only(self) -> bool:
         """No transfer or commit crosses GPUs (e.g. every single-GPU run)."""
@@ -993,6 +1030,19 @@ class _Executor:
                         self.alias_origin[t.dst_hid] = o
                 continue
             if (gs, t.src_hid, t.part) in bset:
+                continue
+            ib = self.shift.get(id(t)) if self.shift else None
+            if ib is not None:
+                # copy engine into the receiver's buffer, then an 8-byte token in the group
+                if self.W.owns(gs):
+                    view = self._send_view(gs, t)
+                    n = max(1, view.numel())
+                    _native.call("td_memcpy_2d", stream_handle(self.xstream(gs)), C.c_void_p(ib.writer_ptr), n,
+                                 C.c_void_p(view.data_ptr()), n, n, 1)
+                    sends.append((gs, gd, self._token(gs)))
+                if self.W.owns(gd):
+                    self.buffers[t.dst_hid] = ib.home_view()
+                    recvs.append((gd, gs, self._token(gd)))
                 continue
             if self.W.owns(gs):
                 sends.append((gs, gd, self._send_view(gs, t)))
@@ -1578,7 +1628,7 @@ def _launch(prog, store, policy) -> None:
         cache[key] = "never"
         return
     plan = rec.finish()
-    sets = [] if not ex.inbox else [peer.inbox_set(prog, store.world, ex.gpu)]
+    sets = [] if not (ex.inbox or ex.shift) else [peer.inbox_set(prog, store.world, ex.gpu)]
     plan.extra["credits"] = [(ib, h) for ib in ex.inbox.values() for i, h in ex.credits.items() if i == id(ib)]
     plan.extra["inbox_sets"] = sets
     for st in sets:

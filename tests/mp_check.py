@@ -120,6 +120,34 @@ def main():
         if not any(isinstance(v, tuple) for v in store.__dict__.get("_launch_plans", {}).values()):
             failures.append(f"plan {b.name} {b.machine}: nothing recorded")
 
+    # copy-engine shifts (peer.CE_SHIFTS): transfers after step 0 go by cudaMemcpy into a
+    # persistent buffer on the receiver + 8-byte NCCL tokens / credits; forced on at test
+    # sizes, eagerly and from replayed launch plans, bit-exact against the oracle
+    from paper_2203_08069_b200 import peer as _peer
+    saved_shift = _peer.SHIFT_MIN_BYTES
+    _peer.SHIFT_MIN_BYTES = 0
+    shifted = 0
+    try:
+        for b in (td.cannon(2, 2, dims=(200, 144, 176)), td.cannon(2, 2, dims=(130, 96, 150)),
+                  td.summa(2, 1, dims=(192, 160, 256), chunk=32), td.pumma(2, 2, dims=(96, 80, 112)),
+                  td.solomonik(2, 2, 2, dims=(64, 48, 80))):
+            cin, store = b.prepare(seed=21, mode=0, world=world)
+            out = b.statement.lhs.tensor.name
+            ins = {n: generate(b.statement.tensors()[n].dims, 21, k + 1, 0) for k, n in enumerate(b.input_names)}
+            want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+            for rep in range(5):
+                store.zero(out)
+                td.execute(cin, store)
+                if not np.array_equal(store[out].tensor.data, want):
+                    failures.append(f"ce-shift {b.name} {b.machine} run {rep}")
+            shifted += sum(len(st.by_transfer()) for st in world.inbox_sets.values())
+    finally:
+        _peer.SHIFT_MIN_BYTES = saved_shift
+    if shifted == 0 and size > 1:
+        failures.append("ce-shift: no copy-engine shift used")
+    if rank == 0:
+        print(f"copy-engine shifts in use: {shifted}", flush=True)
+
     # pipelined first step (k-pieces on the transfers and the GEMM leaves), forced on at test sizes
     saved = rt.SPLIT_MIN_BYTES
     rt.SPLIT_MIN_BYTES = 0
