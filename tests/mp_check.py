@@ -298,6 +298,24 @@ def main():
         if not np.array_equal(store[out].tensor.data, want):
             failures.append(f"graph {b.name} {b.machine} eager after replays")
         del cap
+    # a captured launch whose shifts go by copy engine (forced on at test size)
+    from paper_2203_08069_b200 import peer as _peer
+    saved_shift, _peer.SHIFT_MIN_BYTES = _peer.SHIFT_MIN_BYTES, 0
+    try:
+        b = td.cannon(2, 2, dims=(264, 200, 312))
+        cin, store = b.prepare(seed=19, mode=0, world=world)
+        cap = CapturedLaunch(cin, store)
+        ins = {n: generate(b.statement.tensors()[n].dims, 19, k + 1, 0) for k, n in enumerate(b.input_names)}
+        want = np.asarray(seq_eval(td.format_statement(b.statement), b.statement.extents, ins))
+        for rep in range(3):
+            cap.replay()
+            if not np.array_equal(store["C"].tensor.data, want):
+                failures.append(f"graph ce-shift cannon replay {rep}")
+        if not any(st.by_transfer() for st in world.inbox_sets.values()):
+            failures.append("graph ce-shift: no copy-engine shift used")
+        del cap
+    finally:
+        _peer.SHIFT_MIN_BYTES = saved_shift
     import gc
     gc.collect()
     torch.cuda.synchronize()
