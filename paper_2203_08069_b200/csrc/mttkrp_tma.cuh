@@ -1,22 +1,23 @@
-// Stream-K MTTKRP on the per-i GEMM formulation (included by gemm.cu after
-// gemm_tma.cuh):
+// MTTKRP with a stream-K last wave, on the per-i GEMM formulation (included by
+// gemm.cu after gemm_tma.cuh):
 //
 //     T(i, k, j) = sum_l B(i, k, l) D(l, j)        (DMMA.8x8x4, M = k rows, N = j, K = l)
 //     A(i, j)   (+)= sum_k C(k, j) T(i, k, j)      (row-sum epilogue)
 //
-// An item is one (i, 128 k-rows, 32 j) tile -- B(i, k0:k0+128, :) is one
-// contiguous 1 MB run -- and a unit is one BK-wide l-tile of an item.  The
-// grid is exactly one wave of resident CTAs; CTA c walks the contiguous
-// units [c U / G, (c+1) U / G) of all U = items x l-tiles, with ONE TMA ring
-// running across item boundaries (no per-item prologue, no last-wave tail:
-// the per-i kernel's 8192 short CTAs in 18.5 waves lost ~1.7 % to the tail
-// alone).  At each item end (or the end of its range) every warp does its own
-// row-sum epilogue -- Hadamard with C, fixed shuffle tree over its 32 rows --
-// and stores a 32-wide partial, no CTA-wide barrier; an item cut by a range
-// boundary (at most two CTAs: G <= items) stores its head in slot 0 and its
-// continuation in slot 1.  `mttkrp_st_reduce` sums, per output, the 4 warp
-// groups of every k-tile in ascending order (slot 0 + slot 1 where the item
-// was cut), in four contiguous quarters combined as (q0 + q1) + (q2 + q3).
+// An item is one (i, BM k-rows, 32 j) tile -- B(i, k0:k0+BM, :) is one
+// contiguous run -- and a unit is one BK-wide l-tile of an item.  The first
+// n_dp blocks (all full waves of resident CTAs but the last) take one whole
+// item each; the last n_sk blocks (one per resident slot) walk equal
+// contiguous runs [c U / n_sk, (c+1) U / n_sk) of the remaining U units with
+// ONE TMA ring running across item boundaries, so the last wave has no tail
+// (the per-i kernel's 4096-8192 short CTAs lost ~1.5 % to it).  At each item
+// end (or the end of its range) every warp does its own row-sum epilogue --
+// Hadamard with C, fixed shuffle tree over its 32 rows -- and stores a 32-wide
+// partial, no CTA-wide barrier: the item's head (first unit) into the item's
+// slot, a continuation (an sk block starting mid-item) into the block's own
+// slot.  `mttkrp_st_reduce` sums, per output, the warp groups of every k-tile
+// in ascending order (head + the following sk blocks' continuations in block
+// order), in four contiguous quarters combined as (q0 + q1) + (q2 + q3).
 // No atomics: the order is a fixed function of the shape and the resident-CTA
 // count, runs are bitwise reproducible, integer-valued inputs exact.
 //
