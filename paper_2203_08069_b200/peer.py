@@ -26,7 +26,7 @@ whole output box, and the task runs exactly one leaf (so the leaf can
 
 The same buffers carry **copy-engine shifts** in SPMD jobs: a big
 single-destination transfer after step 0 (Cannon's per-step A / B shifts,
-`algorithms.py:118-132`) is a `cudaMemcpy` by the sender straight into the
+`algorithms.py:109-132`) is a `cudaMemcpy` by the sender straight into the
 receiver's buffer over NVLink -- no NCCL kernel holding SM slots while the
 DMMA waves run -- followed by an 8-byte NCCL token the receiver's step waits
 for; an 8-byte credit at the end of the launch orders the next launch's copy
