@@ -12,6 +12,8 @@
 // .v2.f64), several in flight per lane; reductions are fixed-order
 // (shuffle-xor trees, per-CTA partials then one ordered pass) so results are
 // bitwise reproducible run to run.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace td {
@@ -160,6 +162,92 @@ __global__ void __launch_bounds__(IP_THREADS) innerprod_partial(int64_t rows, in
 }
 
 // pass 2: fixed-order tree over the partials
+// Contiguous operands: the same tiling with the tiles staged by the copy engine
+// (cp.async.bulk, one 32 KiB copy per operand per stage, 3-stage mbarrier ring,
+// one 512-thread block per SM) -- the SMs issue no global loads at all.  Block
+// b owns full tiles b, b + G, ...; block 0 also adds the < IPB_CHUNK tail.
+constexpr int IPB_CHUNK = 4096;   // doubles per operand per stage
+constexpr int IPB_STAGES = 3;
+constexpr int IPB_THREADS = 512;
+constexpr int IPB_SMEM = IPB_STAGES * 2 * IPB_CHUNK * 8 + 128;
+
+__device__ __forceinline__ uint32_t ipb_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(IPB_THREADS, 1) innerprod_bulk(int64_t total, const double* __restrict__ B,
+                                                                 const double* __restrict__ C,
+                                                                 double* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char ipb_raw[];
+  __shared__ __align__(8) uint64_t full[IPB_STAGES], empty[IPB_STAGES];
+  __shared__ double sh[32];
+  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ipb_raw) + 127) & ~uintptr_t(127));
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t nfull = total / IPB_CHUNK;
+  const int64_t G = gridDim.x;
+  const int mine = int((nfull - blockIdx.x + G - 1) / G);   // full tiles of this block
+  if (tid == 0) {
+    for (int s = 0; s < IPB_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ipb_smem(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(ipb_smem(&empty[s])), "r"(IPB_THREADS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int q) {
+    const int s = q % IPB_STAGES;
+    const int64_t off = (int64_t(blockIdx.x) + int64_t(q) * G) * IPB_CHUNK;
+    const uint32_t bar = ipb_smem(&full[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(2 * IPB_CHUNK * 8)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     ipb_smem(sm + (2 * s) * IPB_CHUNK)),
+                 "l"(B + off), "r"(IPB_CHUNK * 8), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     ipb_smem(sm + (2 * s + 1) * IPB_CHUNK)),
+                 "l"(C + off), "r"(IPB_CHUNK * 8), "r"(bar)
+                 : "memory");
+  };
+  auto wait = [](uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                   " selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done)
+                   : "r"(ipb_smem(bar)), "r"(parity)
+                   : "memory");
+    } while (!done);
+  };
+  if (tid == 0)
+    for (int q = 0; q < IPB_STAGES && q < mine; ++q) issue(q);
+  double a0 = 0.0, a1 = 0.0;
+  for (int q = 0; q < mine; ++q) {
+    const int s = q % IPB_STAGES;
+    wait(&full[s], (q / IPB_STAGES) & 1);
+    const double2* vb = reinterpret_cast<const double2*>(sm + (2 * s) * IPB_CHUNK);
+    const double2* vc = reinterpret_cast<const double2*>(sm + (2 * s + 1) * IPB_CHUNK);
+#pragma unroll
+    for (int i = tid; i < IPB_CHUNK / 2; i += 2 * IPB_THREADS) {
+      const double2 b0 = vb[i], c0 = vc[i], b1 = vb[i + IPB_THREADS], c1 = vc[i + IPB_THREADS];
+      a0 = fma(b0.x, c0.x, a0);
+      a0 = fma(b0.y, c0.y, a0);
+      a1 = fma(b1.x, c1.x, a1);
+      a1 = fma(b1.y, c1.y, a1);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(ipb_smem(&empty[s])) : "memory");
+    if (tid == 0 && q + IPB_STAGES < mine) {
+      wait(&empty[s], (q / IPB_STAGES) & 1);   // every warp has read slot s
+      issue(q + IPB_STAGES);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int64_t e = nfull * IPB_CHUNK + tid; e < total; e += IPB_THREADS) a1 = fma(B[e], C[e], a1);
+  const double sum = block_sum(a0 + a1, sh);
+  if (tid == 0) work[blockIdx.x] = sum;
+}
+
 __global__ void __launch_bounds__(1024) innerprod_final(const double* __restrict__ work, int nparts,
                                                         double* out, int accumulate) {
   __shared__ double sh[32];
@@ -274,7 +362,18 @@ int td_innerprod(void* stream, int64_t rows, int64_t n, const double* B, int64_t
   // 8192-element tiles (64 KiB per operand), interleaved over the blocks
   const int64_t chunk = 8192;
   parts = (int)std::max<int64_t>(1, std::min<int64_t>(parts, ceil_div(total, chunk)));
-  if (total > 0) {
+  static const bool bulk_on = [] {
+    const char* e = std::getenv("TD_IP_BULK");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const bool contiguous = (rows == 1 || (sB == n && sC == n)) && (reinterpret_cast<uintptr_t>(B) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+  if (bulk_on && contiguous && total >= int64_t(IPB_CHUNK) * num_sms()) {
+    parts = num_sms();
+    TD_CUDA(ensure_smem(innerprod_bulk, IPB_SMEM));
+    innerprod_bulk<<<parts, IPB_THREADS, IPB_SMEM, st>>>(total, B, C, work);
+    if (int rc = check_launch("innerprod_bulk")) return rc;
+  } else if (total > 0) {
     innerprod_partial<<<parts, IP_THREADS, 0, st>>>(rows, n, B, sB, C, sC, work, chunk);
     int rc = check_launch("innerprod_partial");
     if (rc) return rc;
