@@ -248,6 +248,112 @@ __global__ void __launch_bounds__(IPB_THREADS, 1) innerprod_bulk(int64_t total, 
   if (tid == 0) work[blockIdx.x] = sum;
 }
 
+// TTV on contiguous rows of K in {512, 1024, 2048, 4096}: tiles of 8192
+// doubles (8192 / K whole rows) staged by the copy engine into a 3-stage
+// mbarrier ring, c resident in shared memory, 16 warps per block, one block
+// per SM.  Warp w sums 512 consecutive elements of one row (lane FMAs +
+// shuffle tree) into part[.][w]; the issuing thread, which waits for every
+// warp to release a slot before refilling it, adds each row's segment sums in
+// ascending order and writes A.
+constexpr int TVB_CHUNK = 8192;            // doubles per tile (64 KiB)
+constexpr int TVB_STAGES = 3;
+constexpr int TVB_EPW = TVB_CHUNK / (IPB_THREADS / 32);   // elements per warp and tile (512)
+constexpr int TVB_SMEM = TVB_STAGES * TVB_CHUNK * 8 + 4096 * 8 + 128;
+
+__global__ void __launch_bounds__(IPB_THREADS, 1) ttv_bulk(int64_t rows, int64_t J, int K, const double* __restrict__ B,
+                                                           const double* __restrict__ c, double* __restrict__ A,
+                                                           int64_t sAi, int64_t sAj, int accumulate) {
+  extern __shared__ __align__(128) unsigned char tvb_raw[];
+  __shared__ __align__(8) uint64_t full[TVB_STAGES], empty[TVB_STAGES];
+  __shared__ double part[2 * TVB_STAGES][IPB_THREADS / 32];   // by q % (2 STAGES): never reused before read
+  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tvb_raw) + 127) & ~uintptr_t(127));
+  double* cs = sm + TVB_STAGES * TVB_CHUNK;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int WARPS = IPB_THREADS / 32;
+  const int rpt = TVB_CHUNK / K;            // rows per tile
+  const int wpr = WARPS / rpt;              // warps per row
+  const int64_t tiles = rows / rpt;
+  const int64_t G = gridDim.x;
+  const int mine = int((tiles - blockIdx.x + G - 1) / G);
+  for (int k = tid; k < K; k += IPB_THREADS) cs[k] = c[k];
+  if (tid == 0) {
+    for (int s = 0; s < TVB_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ipb_smem(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(ipb_smem(&empty[s])), "r"(WARPS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int q) {
+    const int s = q % TVB_STAGES;
+    const uint32_t bar = ipb_smem(&full[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(TVB_CHUNK * 8) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     ipb_smem(sm + s * TVB_CHUNK)),
+                 "l"(B + (int64_t(blockIdx.x) + int64_t(q) * G) * TVB_CHUNK), "r"(TVB_CHUNK * 8), "r"(bar)
+                 : "memory");
+  };
+  auto wait = [](uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                   " selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done)
+                   : "r"(ipb_smem(bar)), "r"(parity)
+                   : "memory");
+    } while (!done);
+  };
+  const bool flat = sAi == J * sAj;          // A rows flatten: no division per row
+  auto finish = [&](int q) {  // thread 0, after every warp released stage q's slot
+    const int pq = q % (2 * TVB_STAGES);
+    const int64_t r0 = (int64_t(blockIdx.x) + int64_t(q) * G) * rpt;
+    for (int rr = 0; rr < rpt; ++rr) {
+      double v = 0.0;
+      for (int g = 0; g < wpr; ++g) v += part[pq][rr * wpr + g];
+      const int64_t r = r0 + rr;
+      double* dst = flat ? A + r * sAj : A + (r / J) * sAi + (r - (r / J) * J) * sAj;
+      *dst = accumulate ? *dst + v : v;
+    }
+  };
+  if (tid == 0)
+    for (int q = 0; q < TVB_STAGES && q < mine; ++q) issue(q);
+  const int row_in_tile = warp / wpr;
+  const int k0 = (warp % wpr) * TVB_EPW + 2 * lane;
+  for (int q = 0; q < mine; ++q) {
+    const int s = q % TVB_STAGES;
+    wait(&full[s], (q / TVB_STAGES) & 1);
+    const double* rowp = sm + s * TVB_CHUNK + row_in_tile * K;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < TVB_EPW / 64; u += 2) {
+      const double2 b0 = *reinterpret_cast<const double2*>(rowp + k0 + 64 * u);
+      const double2 b1 = *reinterpret_cast<const double2*>(rowp + k0 + 64 * (u + 1));
+      const double2 c0 = *reinterpret_cast<const double2*>(cs + k0 + 64 * u);
+      const double2 c1 = *reinterpret_cast<const double2*>(cs + k0 + 64 * (u + 1));
+      s0 = fma(b0.x, c0.x, s0);
+      s0 = fma(b0.y, c0.y, s0);
+      s1 = fma(b1.x, c1.x, s1);
+      s1 = fma(b1.y, c1.y, s1);
+    }
+    const double w = warp_sum(s0 + s1);
+    if (lane == 0) {
+      part[q % (2 * TVB_STAGES)][warp] = w;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(ipb_smem(&empty[s])) : "memory");
+    }
+    if (tid == 0 && q >= 1) {  // the previous stage: every warp is past it by now
+      const int p = q - 1;
+      wait(&empty[p % TVB_STAGES], (p / TVB_STAGES) & 1);
+      if (p + TVB_STAGES < mine) issue(p + TVB_STAGES);
+      finish(p);
+    }
+  }
+  if (tid == 0 && mine > 0) {
+    const int p = mine - 1;
+    wait(&empty[p % TVB_STAGES], (p / TVB_STAGES) & 1);
+    finish(p);
+  }
+}
+
 __global__ void __launch_bounds__(1024) innerprod_final(const double* __restrict__ work, int nparts,
                                                         double* out, int accumulate) {
   __shared__ double sh[32];
@@ -345,6 +451,18 @@ int td_ttv(void* stream, int64_t I, int64_t J, int64_t K, const double* B, int64
                    (reinterpret_cast<uintptr_t>(c) & 15) == 0 && sBi % 2 == 0 && sBj % 2 == 0;
   const int64_t want = ceil_div(rows, 8);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
+  static const bool bulk_on = [] {
+    const char* e = std::getenv("TD_TTV_BULK");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const bool rows_contiguous = sBj == K && (I == 1 || sBi == J * K);
+  if (bulk_on && vec && rows_contiguous && K >= TVB_EPW && K <= 4096 && TVB_CHUNK % K == 0 &&
+      rows % (TVB_CHUNK / K) == 0 && rows / (TVB_CHUNK / K) >= 4 * num_sms() &&
+      (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+    TD_CUDA(ensure_smem(ttv_bulk, TVB_SMEM));
+    ttv_bulk<<<num_sms(), IPB_THREADS, TVB_SMEM, as_stream(stream)>>>(rows, J, (int)K, B, c, A, sAi, sAj, accumulate);
+    return check_launch("ttv_bulk");
+  }
   if (vec) ttv_kernel<true><<<blocks, 256, 0, as_stream(stream)>>>(I, J, K, B, sBi, sBj, c, A, sAi, sAj, accumulate);
   else ttv_kernel<false><<<blocks, 256, 0, as_stream(stream)>>>(I, J, K, B, sBi, sBj, c, A, sAi, sAj, accumulate);
   return check_launch("ttv_kernel");

@@ -131,6 +131,24 @@ def test_ttv_exact(nat, i, j, k):
     assert np.array_equal(ta.cpu().numpy(), ref.ttv(b, c))
 
 
+@pytest.mark.parametrize("i,j,k,pad", [(64, 128, 1024, 0), (80, 128, 512, 0), (16, 80, 4096, 0), (64, 128, 1024, 3),
+                                       (1, 2048, 2048, 0)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_ttv_bulk_exact(nat, i, j, k, pad, accumulate):
+    """Contiguous rows large enough for the copy-engine-staged TTV (ttv_bulk:
+    64 KiB tiles of whole rows, K = 512 / 1024 / 2048 / 4096), A flat or with
+    padded rows (pad > 0: the per-row (i, j) address path), += and =, exact."""
+    rng = np.random.default_rng(i + j + k + pad + accumulate)
+    b, c = ints(rng, i, j, k), ints(rng, k)
+    a0 = ints(rng, i, j + pad)
+    tb, tcv, ta = dev(b), dev(c), dev(a0)
+    nat.call("td_ttv", stream(), i, j, k, ptr(tb), j * k, k, ptr(tcv), ptr(ta), j + pad, 1, accumulate)
+    got = ta.cpu().numpy()
+    want = ref.ttv(b, c) + (a0[:, :j] if accumulate else 0)
+    assert np.array_equal(got[:, :j], want)
+    assert np.array_equal(got[:, j:], a0[:, j:])          # padding untouched
+
+
 @pytest.mark.parametrize("i,j,k,l", [(5, 4, 6, 3), (3, 7, 33, 64), (16, 16, 128, 64), (2, 3, 5, 70)])
 def test_ttm_exact(nat, i, j, k, l):
     rng = np.random.default_rng(i * j + k * l)
