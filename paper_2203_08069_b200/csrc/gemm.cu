@@ -414,7 +414,8 @@ static int zero_or_keep(cudaStream_t st, int64_t batch, int64_t M, int64_t N, do
 //   + fixed-address load path, 64x128x16 (cuBLAS's own d884 tile)       35.2
 //   64x64x16, 4 warps of 32x32, 4 stages, 3 CTAs/SM (config 20)         35.6
 //   TMA 64x64x16, 3 stages, 4 CTAs/SM (<= 128 registers; config 47)     36.5  (98.5 %, cuBLAS 36.1)
-// TTM shape (M = 2^20, N = 64, K = 1024): config 20 35.0, config 47 36.0.
+// TTM shape (M = 2^20, N = 64, K = 1024): config 20 35.0, config 47 36.0 (round 2,
+// tools/ttm_configs.py: 47 36.09, 40 (4 stages) 35.79, 50 (128x64) 35.52).
 // N <= 32 (MTTKRP / TTM with a rank-32 factor; the A panel streams from HBM
 // at ~4.4 TB/s): LDGSTS 128x32x8 4 stages (config 34) 33.6, TMA 128x32x16
 // 3 stages (config 48) 35.2.  Also measured at N = 32 (round 1, no gain):
